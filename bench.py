@@ -1,0 +1,440 @@
+#!/usr/bin/env python
+"""Quest decode-attention benchmark (BASELINE.json metric) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1], the headline): Llama-2-7B attention shape -- 32 heads
+(MHA), head_dim 128, page size 16 -- at 32K context with a 2048-token budget, batch 1 per
+GPU, fp16 K/V/q with synthetic N(0, 1/d) data.  One *step* is one decode step through
+NL = 32 independent layer caches (a model's worth of layers): for every layer, append the
+new token's K/V (fused metadata update) -> estimate -> top-K -> sparse attend + LSE merge,
+captured once in a CUDA graph.  `value` is microseconds per layer (step time / NL).  The
+32 layer caches are 17 GB, so every layer's 67 MB working set comes from HBM, not L2
+(each layer is revisited only after 31 other layers have streamed ~2 GB through L2).
+
+N > 1 (torchrun): each rank serves its own request (weak scaling, no collective on the
+attention path); the step time is the max over ranks and `value` is the whole job's time
+per layer-step: max_time / (NL * N).
+
+--impl reference: the reference's own CPU implementation (oracle/_ref, compiled from
+/root/reference) of the same path on the host cores: estimate_all -> select_top_k ->
+sparse_attention for all 32 heads of a layer via questkv::parallel_for.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Quest attn decode latency us/layer @32K ctx, 2048 budget; achieved HBM GB/s"
+UNIT = "us/layer"
+HEADS, HEAD_DIM, PAGE, CTX, BUDGET, LAYERS = 32, 128, 16, 32768, 2048, 32
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--ctx", type=int, default=CTX)
+    ap.add_argument("--budget", type=int, default=BUDGET)
+    ap.add_argument("--layers", type=int, default=LAYERS)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def algorithmic_bytes(lengths, heads, head_dim, page, budget, bpe=2):
+    """Reference byte accounting (metrics.cpp:90-108) for one layer step: per head,
+    metadata 2*d*bpe per page + K/V 2*d*bpe per attended token (the selected pages'
+    actual lengths; force-recent keeps the possibly partial newest page)."""
+    total = 0
+    vec = head_dim * bpe
+    for L in lengths:
+        P = (L + page - 1) // page
+        k = budget // page
+        last_len = L - (P - 1) * page
+        if k >= P:
+            attended = L
+        else:
+            attended = (k - 1) * page + last_len  # top-(K-1) full pages + the newest page
+        total += heads * (2 * vec * P + 2 * vec * attended)
+    return total
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                self.samples.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        sm = [float(s[0]) for s in self.samples if len(s) >= 7 and s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if len(s) >= 7 and s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            if len(s) >= 7:
+                for n, v in zip(names, s[3:7]):
+                    if v.lower() == "active":
+                        reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.samples)}
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (burst copy)"
+    return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+def profiled_traffic():
+    """dram bytes per launch of the decode step from the committed ncu summary, if any."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return json.load(f).get("dram_bytes_per_layer_step")
+    return None
+
+
+def cpu_baseline_sample(ctx, budget, threads, reps=2):
+    """The reference (oracle/_ref) on one full layer: 32 heads at `ctx` tokens."""
+    from oracle import REF_SO, Oracle, Reference  # checker / baseline only
+
+    rng = np.random.default_rng(1)
+    sd = 1.0 / np.sqrt(HEAD_DIM)
+    keys = (rng.standard_normal((HEADS, ctx, HEAD_DIM), dtype=np.float32) * sd)
+    keys = keys.astype(np.float16).astype(np.float32)
+    vals = (rng.standard_normal((HEADS, ctx, HEAD_DIM), dtype=np.float32) * sd)
+    vals = vals.astype(np.float16).astype(np.float32)
+    q = (rng.standard_normal((HEADS, HEAD_DIM)) * sd).astype(np.float16).astype(np.float32)
+    if os.path.exists(REF_SO):
+        ref = Reference()
+        layer = ref.layer(keys, vals, PAGE)
+        mean_ns, min_ns, _ = layer.step(q, budget, threads=threads, warmup=1, reps=reps)
+        layer.close()
+        kind = "reference"
+    else:  # the C restatement, one head at a time (single thread)
+        orc = Oracle()
+        t0 = time.perf_counter()
+        for h in range(HEADS):
+            orc.quest_step(q[h], keys[h], vals[h], PAGE, budget)
+        mean_ns = (time.perf_counter() - t0) * 1e9
+        kind, threads = "port", 1
+    return {"value": mean_ns / 1e3, "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": f"1 layer = {HEADS} heads x {ctx} tokens, d={HEAD_DIM}, S={PAGE}, "
+                      f"budget {budget}; estimate_all->select_top_k->sparse_attention per head "
+                      f"via questkv::parallel_for; mean of {reps} reps after 1 warmup"}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    from oracle import REF_SO, Reference
+
+    if not os.path.exists(REF_SO):
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return
+    rng = np.random.default_rng(1)
+    sd = 1.0 / np.sqrt(HEAD_DIM)
+    keys = (rng.standard_normal((HEADS, args.ctx, HEAD_DIM), dtype=np.float32) * sd)
+    keys = keys.astype(np.float16).astype(np.float32)
+    vals = (rng.standard_normal((HEADS, args.ctx, HEAD_DIM), dtype=np.float32) * sd)
+    vals = vals.astype(np.float16).astype(np.float32)
+    q = (rng.standard_normal((HEADS, HEAD_DIM)) * sd).astype(np.float16).astype(np.float32)
+    layer = Reference().layer(keys, vals, PAGE)
+    steps = max(1, min(args.steps, 20))
+    mean_ns, min_ns, _ = layer.step(q, args.budget, threads=threads, warmup=max(1, min(args.warmup, 3)),
+                                    reps=steps)
+    layer.close()
+    us = mean_ns / 1e3
+    line = {
+        "metric": METRIC, "value": round(us, 3), "unit": UNIT, "impl": "reference",
+        "n_gpus": args.gpus, "steps": steps, "warmup": max(1, min(args.warmup, 3)),
+        "ms_per_step": round(mean_ns / 1e6, 4), "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic N(0,1/d) fp16-representable",
+        "config": {"workload": "cfg2: Llama-2-7B attention (32 heads, d=128, S=16), 32K ctx, "
+                               "budget 2048, batch 1; one layer per step on the host CPU",
+                   "seq_len": args.ctx, "budget": args.budget, "heads": HEADS},
+        "cpu_baseline": {"value": round(us, 3), "unit": UNIT, "cores": threads,
+                         "kind": "reference",
+                         "sample": f"every step = 1 full layer ({HEADS} heads x {args.ctx} tokens)"},
+        "e2e": {"value": round(us, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "min_us_per_layer": round(min_ns / 1e3, 3),
+    }
+    print(json.dumps(line))
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2406_10774_b200 import QuestCache
+
+    rank, world, local = dist_env()
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    NL, ctx, budget = args.layers, args.ctx, args.budget
+    headroom = args.warmup + args.steps + args.e2e_steps + 8
+    qc = QuestCache(HEAD_DIM, PAGE, num_layers=NL, max_batch=1, num_q_heads=HEADS,
+                    max_tokens=ctx + headroom, device=local)
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234 + rank)
+    sd = 1.0 / HEAD_DIM ** 0.5
+    n0 = ctx - 1  # the first timed step appends token ctx-1 -> a 32K context
+    for layer in range(NL):
+        k = (torch.randn((HEADS, n0, HEAD_DIM), generator=g, device=dev) * sd).half()
+        v = (torch.randn((HEADS, n0, HEAD_DIM), generator=g, device=dev) * sd).half()
+        qc.prefill(layer, 0, k, v)
+        del k, v
+    total_steps = args.warmup + args.steps
+    q = (torch.randn((total_steps, NL, 1, HEADS, HEAD_DIM), generator=g, device=dev) * sd).half()
+    kn = (torch.randn((total_steps, NL, 1, HEADS, HEAD_DIM), generator=g, device=dev) * sd).half()
+    vn = (torch.randn((total_steps, NL, 1, HEADS, HEAD_DIM), generator=g, device=dev) * sd).half()
+    qbuf, kbuf, vbuf = q[0].clone(), kn[0].clone(), vn[0].clone()
+    out = torch.empty((NL, 1, HEADS, HEAD_DIM), dtype=torch.float32, device=dev)
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.Stream(device=dev)
+    # Load every kernel of the step eagerly on a throwaway cache of the same geometry
+    # (lazy module loading must not happen inside the capture).
+    warm = QuestCache(HEAD_DIM, PAGE, num_layers=1, max_batch=1, num_q_heads=HEADS,
+                      max_tokens=ctx + headroom, device=local)
+    warm.prefill(0, 0, kn[0, 0].view(HEADS, 1, HEAD_DIM).contiguous(),
+                 vn[0, 0].view(HEADS, 1, HEAD_DIM).contiguous())
+    warm.decode_step(0, qbuf[0], kbuf[0], vbuf[0], budget, stream=stream)
+    stream.synchronize()
+    warm.close()
+    launches0 = qc.kernel_launches
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=stream):
+        for layer in range(NL):
+            qc.decode_step(layer, qbuf[layer], kbuf[layer], vbuf[layer], budget, out=out[layer],
+                           stream=stream)
+    kernels_per_step = qc.kernel_launches - launches0
+    # Host shadow lengths advanced once during capture; every replay advances the device
+    # lengths by one token per layer.
+
+    def step(i):
+        qbuf.copy_(q[i], non_blocking=True)
+        kbuf.copy_(kn[i], non_blocking=True)
+        vbuf.copy_(vn[i], non_blocking=True)
+        graph.replay()
+
+    # the capture itself did not execute; the first replay appends token ctx-1
+    with torch.cuda.stream(stream):
+        for i in range(args.warmup):
+            step(i)
+    stream.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        with torch.cuda.stream(stream):
+            ev0.record(stream)
+            for i in range(args.warmup, total_steps):
+                step(i)
+            ev1.record(stream)
+        stream.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    elapsed_ms = ev0.elapsed_time(ev1)
+    qc.sync_lengths(stream=stream)  # graph replays advanced only the device lengths
+    qc.check_status(stream=stream)
+    if world > 1:
+        t = torch.tensor([elapsed_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+    ms_per_step = elapsed_ms / args.steps
+    us_per_layer = ms_per_step * 1e3 / NL
+    value = us_per_layer / world
+
+    # Algorithmic bytes of the timed steps (lengths ctx-1+warmup+1 .. ).
+    bytes_total = 0
+    for i in range(args.warmup, total_steps):
+        L = ctx + i  # tokens after this step's append (first replay -> ctx)
+        bytes_total += algorithmic_bytes([L], HEADS, HEAD_DIM, PAGE, budget)
+    bytes_per_layer = bytes_total / args.steps
+    achieved_gbs = bytes_per_layer / (us_per_layer * 1e-6) / 1e9
+    peak, peak_src = measured_peaks()
+
+    # Per-kernel breakdown (one layer, eager, CUDA events) on the current state.
+    breakdown = kernel_breakdown(qc, q[0], NL, budget, stream) if rank == 0 else {}
+
+    # End to end through the public C ABI with host buffers (qk_decode_step_host):
+    # H2D of q/k/v from pinned memory and D2H of the fp32 output inside the timed region.
+    qh = torch.empty((NL, 1, HEADS, HEAD_DIM), dtype=torch.float16).pin_memory()
+    kh = torch.empty_like(qh).pin_memory()
+    vh = torch.empty_like(qh).pin_memory()
+    qh.copy_(q[0].cpu())
+    kh.copy_(kn[0].cpu())
+    vh.copy_(vn[0].cpu())
+    oh = torch.empty((NL, 1, HEADS, HEAD_DIM), dtype=torch.float32).pin_memory()
+    qn, kn_, vn_, on = qh.numpy(), kh.numpy(), vh.numpy(), oh.numpy()
+    e2e_steps = max(1, args.e2e_steps)
+    qc.decode_step_host(0, qn[0], kn_[0], vn_[0], budget, out=on[0], stream=stream)  # warm
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        for layer in range(NL):
+            qc.decode_step_host(layer, qn[layer], kn_[layer], vn_[layer], budget, out=on[layer],
+                                stream=stream)
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_us = e2e_s * 1e6 / (e2e_steps * NL) / world
+    h2d = 3 * HEADS * HEAD_DIM * 2 * NL  # q, k, v fp16 per layer
+    d2h = HEADS * HEAD_DIM * 4 * NL
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        cpu = cpu_baseline_sample(ctx, budget, os.cpu_count() or 1)
+    line = {
+        "metric": METRIC,
+        "value": round(value, 3),
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_per_step, 4),
+        "higher_is_better": False,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "fp16 storage, fp64 estimate, fp32 attention accumulate",
+        "data": "synthetic N(0,1/d) fp16 K/V/q (random-init, generated on device)",
+        "config": {
+            "workload": "cfg2: Llama-2-7B attention shape (32 heads MHA, d=128, page 16), "
+                        "32K context, token budget 2048, batch 1 per GPU; step = append+estimate"
+                        "+top-K+sparse attend over 32 distinct layer caches (CUDA graph)",
+            "seq_len": ctx, "budget": budget, "heads": HEADS, "head_dim": HEAD_DIM,
+            "page_size": PAGE, "layers_per_step": NL, "global_batch": world,
+            "parallelism": f"request-sharded x{world} (no collective)",
+            "l2": "inputs larger than L2: 32 rotating layer caches (17 GB), 67 MB touched per "
+                  "layer, each revisited after ~2 GB of other layers",
+        },
+        "latency_us_per_layer": round(us_per_layer, 3),
+        "achieved_hbm_gbs": round(achieved_gbs, 1),
+        "roofline": {
+            "bound": "hbm", "achieved": round(achieved_gbs, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved_gbs / peak, 4), "traffic": profiled_traffic(),
+            "kernel": "decode step (append+estimate+top-K+attend launches of one layer)",
+            "bytes_per_launch": int(bytes_per_layer),
+            "bytes_model": "reference accounting metrics.cpp:105-106: 2*d*2B per page "
+                           "(metadata) + 2*d*2B per attended token",
+            "peak_source": peak_src,
+        },
+        "kernel_breakdown_us": breakdown,
+        "gpu_launches": int(kernels_per_step * args.steps),
+        "clocks": clocks.summary(),
+        "e2e": {"value": round(e2e_us, 3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h,
+                "path": "qk_decode_step_host (C ABI) per layer, pinned host buffers"},
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def kernel_breakdown(qc, q0, NL, budget, stream):
+    """Device time of each op of one layer (eager, CUDA events, 8 layers each)."""
+    import torch
+
+    res = {}
+    n = min(8, NL)
+    scores = [None] * n
+    sel = [None] * n
+    with torch.cuda.stream(stream):
+        for name in ("estimate", "select_topk", "sparse_attend", "dense_attend"):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for layer in range(n):
+                if name == "estimate":
+                    scores[layer] = qc.estimate(layer, q0[layer], stream=stream)
+                elif name == "select_topk":
+                    sel[layer] = qc.select_topk(layer, scores[layer], budget, stream=stream)
+                elif name == "sparse_attend":
+                    qc.sparse_attend(layer, q0[layer], sel[layer][0], sel[layer][1], stream=stream)
+                else:
+                    qc.dense_attend(layer, q0[layer], stream=stream)
+            e1.record(stream)
+            stream.synchronize()
+            res[name] = round(e0.elapsed_time(e1) * 1e3 / n, 2)
+    return res
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

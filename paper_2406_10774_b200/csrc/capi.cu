@@ -1,0 +1,568 @@
+// capi.cu -- the extern "C" boundary (include/questkv_b200.h): argument validation with
+// the reference's error semantics, cache allocation, and dispatch to the kernels.
+// No exception crosses this boundary; every failure is a status code plus a
+// thread-local message.
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "qk_internal.cuh"
+
+namespace qk {
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+int set_error(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+int cuda_check(cudaError_t err, const char* what) {
+    if (err == cudaSuccess) return QK_OK;
+    return set_error(QK_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(err));
+}
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+int check_layer_batch(const qk_cache* c, uint32_t layer, uint32_t batch, const char* fn) {
+    if (layer >= c->L)
+        return set_error(QK_ERR_OUT_OF_RANGE, std::string(fn) + ": layer out of range");
+    if (batch == 0 || batch > c->B)
+        return set_error(QK_ERR_INVALID_ARGUMENT,
+                         std::string(fn) + ": batch must be in 1..max_batch");
+    return QK_OK;
+}
+
+uint32_t pages_of(const qk_cache* c, uint32_t tokens) { return (tokens + c->S - 1) / c->S; }
+
+// Max page count over sequences [0, batch) of a layer (host shadow); 0 if any is empty
+// and `require_nonempty`.
+uint32_t max_pages(const qk_cache* c, uint32_t layer, uint32_t batch, bool* any_empty) {
+    uint32_t m = 0;
+    *any_empty = false;
+    for (uint32_t b = 0; b < batch; ++b) {
+        const uint32_t t = c->h_len[size_t(layer) * c->B + b];
+        if (t == 0) *any_empty = true;
+        const uint32_t p = pages_of(c, t);
+        m = p > m ? p : m;
+    }
+    return m;
+}
+
+template <typename T>
+int dmalloc(qk_cache* c, T** p, size_t count) {
+    const size_t bytes = count * sizeof(T);
+    const cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), bytes ? bytes : 16);
+    if (e != cudaSuccess) return cuda_check(e, "cudaMalloc");
+    c->device_bytes += bytes;
+    return cuda_check(cudaMemset(*p, 0, bytes ? bytes : 16), "cudaMemset");
+}
+
+void free_cache(qk_cache* c) {
+    void* ptrs[] = {c->k_pool,    c->v_pool,    c->meta,      c->d_len,     c->ws_partial,
+                    c->ws_ticket, c->d_status,  c->ws_scores, c->ws_pages,  c->ws_counts,
+                    c->ws_io,     c->ws_out,    c->len_ticket, c->probe};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    delete c;
+}
+
+}  // namespace
+}  // namespace qk
+
+using namespace qk;
+
+extern "C" {
+
+const char* qk_last_error(void) { return g_last_error.c_str(); }
+int qk_abi_version(void) { return QK_ABI_VERSION; }
+
+int qk_cache_create(const qk_cache_desc* desc, qk_cache** out) {
+    if (!desc || !out) return set_error(QK_ERR_INVALID_ARGUMENT, "qk_cache_create: null argument");
+    *out = nullptr;
+    // CacheConfig::validate, kv_store.cpp:8-13 (same messages).
+    if (desc->head_dim == 0)
+        return set_error(QK_ERR_INVALID_ARGUMENT, "CacheConfig: head_dim must be >= 1");
+    if (desc->page_size == 0)
+        return set_error(QK_ERR_INVALID_ARGUMENT, "CacheConfig: page_size must be >= 1");
+    if (desc->bytes_per_element == 0)
+        return set_error(QK_ERR_INVALID_ARGUMENT, "CacheConfig: bytes_per_element must be >= 1");
+    if (desc->bytes_per_element != 2)
+        return set_error(QK_ERR_UNSUPPORTED, "qk_cache_create: pools are fp16 (bytes_per_element 2)");
+    if (desc->head_dim > 256)
+        return set_error(QK_ERR_UNSUPPORTED, "qk_cache_create: head_dim > 256");
+    if (desc->page_size > 64)
+        return set_error(QK_ERR_UNSUPPORTED, "qk_cache_create: page_size > 64");
+    if (desc->num_layers == 0 || desc->max_batch == 0 || desc->num_q_heads == 0 ||
+        desc->num_kv_heads == 0 || desc->max_tokens == 0)
+        return set_error(QK_ERR_INVALID_ARGUMENT, "qk_cache_create: zero dimension");
+    if (desc->num_q_heads % desc->num_kv_heads != 0)
+        return set_error(QK_ERR_INVALID_ARGUMENT,
+                         "qk_cache_create: num_q_heads must be a multiple of num_kv_heads");
+    const uint32_t G = desc->num_q_heads / desc->num_kv_heads;
+    if (G != 1 && G != 2 && G != 4 && G != 8)
+        return set_error(QK_ERR_UNSUPPORTED, "qk_cache_create: GQA group must be 1, 2, 4 or 8");
+    const uint64_t pmax = (uint64_t(desc->max_tokens) + desc->page_size - 1) / desc->page_size;
+    if (pmax > kMaxPages)
+        return set_error(QK_ERR_UNSUPPORTED, "qk_cache_create: more than 16384 pages per slice");
+
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return set_error(QK_ERR_CUDA, "qk_cache_create: no CUDA device (this library has no CPU path)");
+    if (desc->device < 0 || desc->device >= ndev)
+        return set_error(QK_ERR_INVALID_ARGUMENT, "qk_cache_create: bad device ordinal");
+    DeviceGuard guard(desc->device);
+
+    qk_cache* c = new (std::nothrow) qk_cache;
+    if (!c) return set_error(QK_ERR_CUDA, "qk_cache_create: out of host memory");
+    c->desc = *desc;
+    c->D = desc->head_dim <= 64 ? 64 : (desc->head_dim <= 128 ? 128 : 256);
+    c->S = desc->page_size;
+    c->L = desc->num_layers;
+    c->B = desc->max_batch;
+    c->Hq = desc->num_q_heads;
+    c->Hkv = desc->num_kv_heads;
+    c->G = G;
+    c->Pmax = uint32_t(pmax);
+    c->Ptiles = (c->Pmax + kMetaTile - 1) / kMetaTile;
+    c->slice_kv = size_t(c->Pmax) * c->S * c->D;
+    c->slice_meta = size_t(c->Ptiles) * 2 * c->D * kMetaTile;
+    const size_t slices = size_t(c->L) * c->B * c->Hkv;
+    c->h_len.assign(size_t(c->L) * c->B, 0);
+    int rc = QK_OK;
+    if (!rc) rc = dmalloc(c, &c->k_pool, slices * c->slice_kv);
+    if (!rc) rc = dmalloc(c, &c->v_pool, slices * c->slice_kv);
+    if (!rc) rc = dmalloc(c, &c->meta, slices * c->slice_meta);
+    if (!rc) rc = dmalloc(c, &c->d_len, size_t(c->L) * c->B);
+    if (!rc) rc = dmalloc(c, &c->ws_partial, size_t(c->B) * c->Hq * kMaxSplits * (c->D + 2));
+    if (!rc) rc = dmalloc(c, &c->ws_ticket, size_t(c->B) * c->Hq);
+    if (!rc) rc = dmalloc(c, &c->d_status, 1);
+    if (!rc) rc = dmalloc(c, &c->len_ticket, size_t(c->L) * c->B);
+    if (!rc && getenv("QK_PROBE")) rc = dmalloc(c, &c->probe, size_t(c->B) * c->Hkv * 8 * 16);
+    if (!rc) rc = dmalloc(c, &c->ws_scores, size_t(c->B) * c->Hq * c->Pmax);
+    if (!rc) rc = dmalloc(c, &c->ws_pages, size_t(c->B) * c->Hq * c->Pmax);
+    if (!rc) rc = dmalloc(c, &c->ws_counts, size_t(c->B) * c->Hq);
+    if (!rc) rc = dmalloc(c, &c->ws_io, size_t(c->B) * (c->Hq + 2 * c->Hkv) * desc->head_dim);
+    if (!rc) rc = dmalloc(c, &c->ws_out, size_t(c->B) * c->Hq * desc->head_dim);
+    if (!rc) rc = cuda_check(cudaDeviceSynchronize(), "qk_cache_create");
+    if (rc) {
+        free_cache(c);
+        return rc;
+    }
+    *out = c;
+    return QK_OK;
+}
+
+int qk_cache_destroy(qk_cache* c) {
+    if (!c) return QK_OK;
+    DeviceGuard guard(c->desc.device);
+    cudaDeviceSynchronize();
+    free_cache(c);
+    return QK_OK;
+}
+
+int qk_cache_describe(const qk_cache* c, qk_cache_desc* out) {
+    if (!c || !out) return set_error(QK_ERR_INVALID_ARGUMENT, "qk_cache_describe: null argument");
+    *out = c->desc;
+    return QK_OK;
+}
+
+uint64_t qk_cache_device_bytes(const qk_cache* c) { return c ? c->device_bytes : 0; }
+uint32_t qk_cache_max_pages(const qk_cache* c) { return c ? c->Pmax : 0; }
+uint64_t qk_kernel_launches(const qk_cache* c) { return c ? c->launches.load() : 0; }
+
+int qk_token_count(const qk_cache* c, uint32_t layer, uint32_t seq, uint32_t* count) {
+    if (!c || !count) return set_error(QK_ERR_INVALID_ARGUMENT, "qk_token_count: null argument");
+    if (layer >= c->L || seq >= c->B)
+        return set_error(QK_ERR_OUT_OF_RANGE, "qk_token_count: slice out of range");
+    *count = c->h_len[size_t(layer) * c->B + seq];
+    return QK_OK;
+}
+
+int qk_page_count(const qk_cache* c, uint32_t layer, uint32_t seq, uint32_t* count) {
+    uint32_t t = 0;
+    const int rc = qk_token_count(c, layer, seq, &t);
+    if (rc) return rc;
+    *count = pages_of(c, t);
+    return QK_OK;
+}
+
+int qk_reset(qk_cache* c, uint32_t layer, void* stream) {
+    if (!c) return set_error(QK_ERR_INVALID_ARGUMENT, "qk_reset: null cache");
+    DeviceGuard guard(c->desc.device);
+    if (layer == UINT32_MAX) {
+        std::fill(c->h_len.begin(), c->h_len.end(), 0u);
+        return cuda_check(cudaMemsetAsync(c->d_len, 0, sizeof(int32_t) * c->L * c->B,
+                                          as_stream(stream)),
+                          "qk_reset");
+    }
+    if (layer >= c->L) return set_error(QK_ERR_OUT_OF_RANGE, "qk_reset: layer out of range");
+    std::fill(c->h_len.begin() + size_t(layer) * c->B, c->h_len.begin() + size_t(layer + 1) * c->B, 0u);
+    return cuda_check(cudaMemsetAsync(c->d_len + size_t(layer) * c->B, 0, sizeof(int32_t) * c->B,
+                                      as_stream(stream)),
+                      "qk_reset");
+}
+
+int qk_append(qk_cache* c, uint32_t layer, const uint16_t* k, const uint16_t* v,
+              uint32_t batch, void* stream) {
+    if (!c || !k || !v) return set_error(QK_ERR_INVALID_ARGUMENT, "KvCache::append: null argument");
+    if (int rc = check_layer_batch(c, layer, batch, "KvCache::append")) return rc;
+    for (uint32_t b = 0; b < batch; ++b)
+        if (c->h_len[size_t(layer) * c->B + b] >= c->desc.max_tokens)
+            return set_error(QK_ERR_OUT_OF_RANGE, "KvCache::append: cache slice is full");
+    DeviceGuard guard(c->desc.device);
+    const int rc = launch_append(c, layer, reinterpret_cast<const __half*>(k),
+                                 reinterpret_cast<const __half*>(v), batch, as_stream(stream));
+    if (rc) return rc;
+    for (uint32_t b = 0; b < batch; ++b) c->h_len[size_t(layer) * c->B + b] += 1;
+    return QK_OK;
+}
+
+int qk_prefill(qk_cache* c, uint32_t layer, uint32_t seq, const uint16_t* k, const uint16_t* v,
+               uint32_t n_tokens, void* stream) {
+    if (!c || !k || !v) return set_error(QK_ERR_INVALID_ARGUMENT, "qk_prefill: null argument");
+    if (layer >= c->L || seq >= c->B)
+        return set_error(QK_ERR_OUT_OF_RANGE, "qk_prefill: slice out of range");
+    if (n_tokens == 0) return QK_OK;
+    uint32_t& t = c->h_len[size_t(layer) * c->B + seq];
+    if (uint64_t(t) + n_tokens > c->desc.max_tokens)
+        return set_error(QK_ERR_OUT_OF_RANGE, "qk_prefill: exceeds cache capacity");
+    DeviceGuard guard(c->desc.device);
+    const int rc = launch_prefill(c, layer, seq, reinterpret_cast<const __half*>(k),
+                                  reinterpret_cast<const __half*>(v), n_tokens, t,
+                                  as_stream(stream));
+    if (rc) return rc;
+    t += n_tokens;
+    return QK_OK;
+}
+
+}  // extern "C"
+
+namespace qk {
+namespace readback {
+
+__global__ void gather_meta_kernel(const __half* __restrict__ meta, __half* __restrict__ mn,
+                                   __half* __restrict__ mx, size_t base, uint32_t page0,
+                                   uint32_t n, int D, uint32_t head_dim) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n * head_dim) return;
+    const uint32_t p = page0 + i / head_dim, ch = i % head_dim;
+    const size_t off = base + size_t(p / kMetaTile) * 2 * D * kMetaTile + size_t(ch) * kMetaTile +
+                       (p % kMetaTile);
+    mn[i] = meta[off];
+    mx[i] = meta[off + size_t(D) * kMetaTile];
+}
+
+__global__ void gather_kv_kernel(const __half* __restrict__ kp, const __half* __restrict__ vp,
+                                 __half* __restrict__ ko, __half* __restrict__ vo, size_t base,
+                                 uint32_t t0, uint32_t n, int D, uint32_t head_dim) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n * head_dim) return;
+    const uint32_t t = t0 + i / head_dim, ch = i % head_dim;
+    const size_t off = base + size_t(t) * D + ch;  // token t = page*S + row
+    ko[i] = kp[off];
+    vo[i] = vp[off];
+}
+
+int read_back(qk_cache* c, __half* d0, __half* d1, uint16_t* h0, uint16_t* h1, size_t n,
+              cudaStream_t st) {
+    int rc = cuda_check(cudaMemcpyAsync(h0, d0, n * 2, cudaMemcpyDeviceToHost, st), "read");
+    if (!rc) rc = cuda_check(cudaMemcpyAsync(h1, d1, n * 2, cudaMemcpyDeviceToHost, st), "read");
+    if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "read");
+    return rc;
+}
+
+}  // namespace readback
+}  // namespace qk
+
+using namespace qk::readback;
+
+extern "C" {
+
+int qk_read_metadata(const qk_cache* cc, uint32_t layer, uint32_t seq, uint32_t kv_head,
+                     uint32_t page0, uint32_t n_pages, uint16_t* min_host, uint16_t* max_host,
+                     void* stream) {
+    qk_cache* c = const_cast<qk_cache*>(cc);
+    if (!c || !min_host || !max_host)
+        return set_error(QK_ERR_INVALID_ARGUMENT, "KvCache::page_metadata: null argument");
+    if (layer >= c->L || seq >= c->B || kv_head >= c->Hkv)
+        return set_error(QK_ERR_OUT_OF_RANGE, "KvCache::page_metadata: slice out of range");
+    const uint32_t P = pages_of(c, c->h_len[size_t(layer) * c->B + seq]);
+    if (uint64_t(page0) + n_pages > P)
+        return set_error(QK_ERR_OUT_OF_RANGE, "KvCache::page_metadata: page index " +
+                                                  std::to_string(page0 + n_pages - 1) +
+                                                  " out of range");
+    if (n_pages == 0) return QK_OK;
+    DeviceGuard guard(c->desc.device);
+    cudaStream_t st = as_stream(stream);
+    const size_t n = size_t(n_pages) * c->desc.head_dim;
+    __half* tmp = nullptr;
+    int rc = cuda_check(cudaMalloc(&tmp, 2 * n * sizeof(__half)), "qk_read_metadata");
+    if (rc) return rc;
+    gather_meta_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(
+        c->meta, tmp, tmp + n, c->slice(layer, seq, kv_head) * c->slice_meta, page0, n_pages,
+        c->D, c->desc.head_dim);
+    c->launches++;
+    rc = cuda_check(cudaGetLastError(), "gather_meta_kernel");
+    if (!rc) rc = read_back(c, tmp, tmp + n, min_host, max_host, n, st);
+    cudaFree(tmp);
+    return rc;
+}
+
+int qk_read_kv(const qk_cache* cc, uint32_t layer, uint32_t seq, uint32_t kv_head,
+               uint32_t token0, uint32_t n_tokens, uint16_t* k_host, uint16_t* v_host,
+               void* stream) {
+    qk_cache* c = const_cast<qk_cache*>(cc);
+    if (!c || !k_host || !v_host)
+        return set_error(QK_ERR_INVALID_ARGUMENT, "KvCache::key: null argument");
+    if (layer >= c->L || seq >= c->B || kv_head >= c->Hkv)
+        return set_error(QK_ERR_OUT_OF_RANGE, "KvCache::key: slice out of range");
+    if (uint64_t(token0) + n_tokens > c->h_len[size_t(layer) * c->B + seq])
+        return set_error(QK_ERR_OUT_OF_RANGE, "KvCache::key: token " +
+                                                  std::to_string(token0 + n_tokens - 1) +
+                                                  " out of range");
+    if (n_tokens == 0) return QK_OK;
+    DeviceGuard guard(c->desc.device);
+    cudaStream_t st = as_stream(stream);
+    const size_t n = size_t(n_tokens) * c->desc.head_dim;
+    __half* tmp = nullptr;
+    int rc = cuda_check(cudaMalloc(&tmp, 2 * n * sizeof(__half)), "qk_read_kv");
+    if (rc) return rc;
+    gather_kv_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(
+        c->k_pool, c->v_pool, tmp, tmp + n, c->slice(layer, seq, kv_head) * c->slice_kv, token0,
+        n_tokens, c->D, c->desc.head_dim);
+    c->launches++;
+    rc = cuda_check(cudaGetLastError(), "gather_kv_kernel");
+    if (!rc) rc = read_back(c, tmp, tmp + n, k_host, v_host, n, st);
+    cudaFree(tmp);
+    return rc;
+}
+
+int qk_estimate(const qk_cache* c, uint32_t layer, const uint16_t* q, uint32_t batch,
+                double* scores, uint32_t scores_stride, void* stream) {
+    if (!c || !q || !scores) return set_error(QK_ERR_INVALID_ARGUMENT, "estimate_all: null argument");
+    if (int rc = check_layer_batch(c, layer, batch, "estimate_all")) return rc;
+    bool empty = false;
+    const uint32_t mp = max_pages(c, layer, batch, &empty);
+    if (empty) return set_error(QK_ERR_INVALID_ARGUMENT, "estimate_all: empty cache");
+    if (scores_stride < mp)
+        return set_error(QK_ERR_INVALID_ARGUMENT, "estimate_all: scores_stride below page count");
+    DeviceGuard guard(c->desc.device);
+    return launch_estimate(c, layer, reinterpret_cast<const __half*>(q), batch, scores,
+                           scores_stride, c->Pmax, as_stream(stream));
+}
+
+int qk_select_topk(const qk_cache* c, uint32_t layer, const double* scores,
+                   uint32_t scores_stride, uint32_t batch, const qk_selection_cfg* cfg,
+                   int32_t* pages, uint32_t pages_stride, int32_t* counts, void* stream) {
+    if (!c || !scores || !cfg || !pages || !counts)
+        return set_error(QK_ERR_INVALID_ARGUMENT, "select_top_k: null argument");
+    if (int rc = check_layer_batch(c, layer, batch, "select_top_k")) return rc;
+    bool empty = false;
+    const uint32_t mp = max_pages(c, layer, batch, &empty);
+    qk_selection_cfg eff = *cfg;
+    if (!cfg->per_layer_enabled) {
+        eff.token_budget = UINT32_MAX;  // every page (criticality.cpp:47)
+    } else {
+        if (cfg->token_budget < c->S)
+            return set_error(QK_ERR_INVALID_ARGUMENT, "select_top_k: token_budget below page_size");
+        if (empty) return set_error(QK_ERR_INVALID_ARGUMENT, "select_top_k: no scores");
+    }
+    const uint32_t k = eff.token_budget / c->S;
+    const uint32_t need = k < mp ? k : mp;
+    if (pages_stride < need)
+        return set_error(QK_ERR_INVALID_ARGUMENT, "select_top_k: pages_stride below selection size");
+    if (scores_stride < mp)
+        return set_error(QK_ERR_INVALID_ARGUMENT, "select_top_k: scores_stride below page count");
+    DeviceGuard guard(c->desc.device);
+    return launch_topk(c, layer, scores, scores_stride, batch, eff, pages, pages_stride, counts,
+                       c->Pmax, as_stream(stream));
+}
+
+int qk_sparse_attend(const qk_cache* c, uint32_t layer, const uint16_t* q, uint32_t batch,
+                     const int32_t* pages, uint32_t pages_stride, const int32_t* counts,
+                     void* out, int32_t out_dtype, float* lse, void* stream) {
+    if (!c || !q || !pages || !counts || !out)
+        return set_error(QK_ERR_INVALID_ARGUMENT, "sparse_attention: null argument");
+    if (int rc = check_layer_batch(c, layer, batch, "sparse_attention")) return rc;
+    if (out_dtype != QK_DTYPE_F32 && out_dtype != QK_DTYPE_F16)
+        return set_error(QK_ERR_INVALID_ARGUMENT, "sparse_attention: bad out_dtype");
+    bool empty = false;
+    const uint32_t mp = max_pages(c, layer, batch, &empty);
+    if (empty) return set_error(QK_ERR_INVALID_ARGUMENT, "sparse_attention: empty cache");
+    const uint32_t max_list = pages_stride < c->Pmax ? pages_stride : c->Pmax;
+    DeviceGuard guard(c->desc.device);
+    return launch_attend(c, layer, reinterpret_cast<const __half*>(q), batch, pages, pages_stride,
+                         counts, false, max_list, out, out_dtype, lse, as_stream(stream));
+}
+
+int qk_dense_attend(const qk_cache* c, uint32_t layer, const uint16_t* q, uint32_t batch,
+                    void* out, int32_t out_dtype, float* lse, void* stream) {
+    if (!c || !q || !out) return set_error(QK_ERR_INVALID_ARGUMENT, "full_attention: null argument");
+    if (int rc = check_layer_batch(c, layer, batch, "full_attention")) return rc;
+    if (out_dtype != QK_DTYPE_F32 && out_dtype != QK_DTYPE_F16)
+        return set_error(QK_ERR_INVALID_ARGUMENT, "full_attention: bad out_dtype");
+    bool empty = false;
+    const uint32_t mp = max_pages(c, layer, batch, &empty);
+    if (empty) return set_error(QK_ERR_INVALID_ARGUMENT, "full_attention: empty cache");
+    DeviceGuard guard(c->desc.device);
+    return launch_attend(c, layer, reinterpret_cast<const __half*>(q), batch, nullptr, 0, nullptr,
+                         true, c->Pmax, out, out_dtype, lse, as_stream(stream));
+}
+
+int qk_decode_step(qk_cache* c, uint32_t layer, const uint16_t* q, const uint16_t* k,
+                   const uint16_t* v, uint32_t batch, const qk_selection_cfg* cfg, void* out,
+                   int32_t out_dtype, int32_t* pages_out, uint32_t pages_stride,
+                   int32_t* counts_out, void* stream) {
+    if (!c || !q || !cfg || !out) return set_error(QK_ERR_INVALID_ARGUMENT, "qk_decode_step: null argument");
+    if (int rc = check_layer_batch(c, layer, batch, "qk_decode_step")) return rc;
+    if ((k == nullptr) != (v == nullptr))
+        return set_error(QK_ERR_INVALID_ARGUMENT, "qk_decode_step: k and v must both be given");
+    if (out_dtype != QK_DTYPE_F32 && out_dtype != QK_DTYPE_F16)
+        return set_error(QK_ERR_INVALID_ARGUMENT, "qk_decode_step: bad out_dtype");
+    if (cfg->per_layer_enabled && cfg->token_budget < c->S)
+        return set_error(QK_ERR_INVALID_ARGUMENT, "select_top_k: token_budget below page_size");
+    const uint32_t add = k ? 1 : 0;
+    bool empty = false;
+    for (uint32_t b = 0; b < batch; ++b) {
+        const uint32_t t = c->h_len[size_t(layer) * c->B + b];
+        if (t + add > c->desc.max_tokens)
+            return set_error(QK_ERR_OUT_OF_RANGE, "KvCache::append: cache slice is full");
+        if (t + add == 0) empty = true;
+    }
+    if (empty) return set_error(QK_ERR_INVALID_ARGUMENT, "estimate_all: empty cache");
+    uint32_t mp = 0;
+    for (uint32_t b = 0; b < batch; ++b) {
+        const uint32_t p = pages_of(c, c->h_len[size_t(layer) * c->B + b] + add);
+        mp = p > mp ? p : mp;
+    }
+    if (pages_out) {
+        const uint32_t kk = cfg->per_layer_enabled ? cfg->token_budget / c->S : UINT32_MAX;
+        const uint32_t need = kk < mp ? kk : mp;
+        if (pages_stride < need)
+            return set_error(QK_ERR_INVALID_ARGUMENT, "qk_decode_step: pages_stride below selection size");
+    }
+    DeviceGuard guard(c->desc.device);
+    const int rc = launch_decode(c, layer, reinterpret_cast<const __half*>(q),
+                                 reinterpret_cast<const __half*>(k),
+                                 reinterpret_cast<const __half*>(v), batch, *cfg, c->Pmax, out,
+                                 out_dtype, pages_out, pages_stride, counts_out,
+                                 as_stream(stream));
+    if (rc) return rc;
+    if (add)
+        for (uint32_t b = 0; b < batch; ++b) c->h_len[size_t(layer) * c->B + b] += 1;
+    return QK_OK;
+}
+
+int qk_decode_step_host(qk_cache* c, uint32_t layer, const uint16_t* q_host,
+                        const uint16_t* k_host, const uint16_t* v_host, uint32_t batch,
+                        const qk_selection_cfg* cfg, float* out_host, void* stream) {
+    if (!c || !q_host || !cfg || !out_host)
+        return set_error(QK_ERR_INVALID_ARGUMENT, "qk_decode_step_host: null argument");
+    if (int rc = check_layer_batch(c, layer, batch, "qk_decode_step_host")) return rc;
+    if ((k_host == nullptr) != (v_host == nullptr))
+        return set_error(QK_ERR_INVALID_ARGUMENT, "qk_decode_step_host: k and v must both be given");
+    DeviceGuard guard(c->desc.device);
+    cudaStream_t st = as_stream(stream);
+    const size_t hd = c->desc.head_dim;
+    const size_t nq = size_t(batch) * c->Hq * hd, nkv = size_t(batch) * c->Hkv * hd;
+    uint16_t* dq = c->ws_io;
+    uint16_t* dk = dq + nq;
+    uint16_t* dv = dk + nkv;
+    int rc = cuda_check(cudaMemcpyAsync(dq, q_host, nq * 2, cudaMemcpyHostToDevice, st), "h2d q");
+    if (!rc && k_host) {
+        rc = cuda_check(cudaMemcpyAsync(dk, k_host, nkv * 2, cudaMemcpyHostToDevice, st), "h2d k");
+        if (!rc) rc = cuda_check(cudaMemcpyAsync(dv, v_host, nkv * 2, cudaMemcpyHostToDevice, st), "h2d v");
+    }
+    if (!rc)
+        rc = qk_decode_step(c, layer, dq, k_host ? dk : nullptr, k_host ? dv : nullptr, batch, cfg,
+                            c->ws_out, QK_DTYPE_F32, nullptr, 0, nullptr, stream);
+    if (!rc)
+        rc = cuda_check(cudaMemcpyAsync(out_host, c->ws_out, size_t(batch) * c->Hq * hd * 4,
+                                        cudaMemcpyDeviceToHost, st),
+                        "d2h out");
+    if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "qk_decode_step_host");
+    return rc;
+}
+
+int qk_debug_probe(qk_cache* c, uint64_t* host, uint32_t n, void* stream) {
+    if (!c || !host) return set_error(QK_ERR_INVALID_ARGUMENT, "qk_debug_probe: null argument");
+    if (!c->probe) return set_error(QK_ERR_INVALID_ARGUMENT, "qk_debug_probe: set QK_PROBE=1 before qk_cache_create");
+    const size_t cap = size_t(c->B) * c->Hkv * 8 * 16;
+    const size_t cnt = n < cap ? n : cap;
+    DeviceGuard guard(c->desc.device);
+    cudaStream_t st = as_stream(stream);
+    int rc = cuda_check(cudaMemcpyAsync(host, c->probe, cnt * 8, cudaMemcpyDeviceToHost, st), "probe");
+    if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "probe");
+    return rc;
+}
+
+int qk_debug_step_scores(qk_cache* c, uint32_t seq, uint32_t q_head, double* host, uint32_t n,
+                         void* stream) {
+    if (!c || !host) return set_error(QK_ERR_INVALID_ARGUMENT, "qk_debug_step_scores: null argument");
+    if (seq >= c->B || q_head >= c->Hq || n > c->Pmax)
+        return set_error(QK_ERR_OUT_OF_RANGE, "qk_debug_step_scores: out of range");
+    DeviceGuard guard(c->desc.device);
+    cudaStream_t st = as_stream(stream);
+    int rc = cuda_check(cudaMemcpyAsync(host, c->ws_scores + (size_t(seq) * c->Hq + q_head) * c->Pmax,
+                                        size_t(n) * 8, cudaMemcpyDeviceToHost, st), "scores");
+    if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "scores");
+    return rc;
+}
+
+int qk_sync_lengths(qk_cache* c, void* stream) {
+    if (!c) return set_error(QK_ERR_INVALID_ARGUMENT, "qk_sync_lengths: null cache");
+    DeviceGuard guard(c->desc.device);
+    cudaStream_t st = as_stream(stream);
+    std::vector<int32_t> tmp(size_t(c->L) * c->B);
+    int rc = cuda_check(cudaMemcpyAsync(tmp.data(), c->d_len, tmp.size() * 4,
+                                        cudaMemcpyDeviceToHost, st), "qk_sync_lengths");
+    if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "qk_sync_lengths");
+    if (rc) return rc;
+    for (size_t i = 0; i < tmp.size(); ++i) c->h_len[i] = uint32_t(tmp[i]);
+    return QK_OK;
+}
+
+int qk_check_status(qk_cache* c, void* stream) {
+    if (!c) return set_error(QK_ERR_INVALID_ARGUMENT, "qk_check_status: null cache");
+    DeviceGuard guard(c->desc.device);
+    cudaStream_t st = as_stream(stream);
+    int32_t code = 0;
+    int rc = cuda_check(cudaMemcpyAsync(&code, c->d_status, 4, cudaMemcpyDeviceToHost, st), "status");
+    if (!rc) rc = cuda_check(cudaMemsetAsync(c->d_status, 0, 4, st), "status");
+    if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "status");
+    if (rc) return rc;
+    switch (code) {
+        case QK_DEV_OK: return QK_OK;
+        case QK_DEV_PAGE_OUT_OF_RANGE:
+            return set_error(QK_ERR_OUT_OF_RANGE, "sparse_attention: page index out of range");
+        case QK_DEV_PAGE_NOT_ASCENDING:
+            return set_error(QK_ERR_INVALID_ARGUMENT,
+                             "sparse_attention: page list not strictly ascending (duplicate page index)");
+        case QK_DEV_EMPTY_SELECTION:
+            return set_error(QK_ERR_INVALID_ARGUMENT, "sparse_attention: empty page selection");
+        case QK_DEV_CAPACITY:
+            return set_error(QK_ERR_OUT_OF_RANGE, "KvCache::append: cache slice is full");
+        default: return set_error(QK_ERR_CUDA, "unknown device status");
+    }
+}
+
+}  // extern "C"

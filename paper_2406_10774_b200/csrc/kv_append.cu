@@ -1,0 +1,133 @@
+// kv_append.cu -- KvCache::append with the page-metadata update fused in (K1), the
+// page-parallel bulk prefill, and the read-back gathers used by the parity tests.
+//
+// Reference: KvCache::append, /root/reference/proj/core/src/kv_store.cpp:19-47.
+//   token t -> page t/S, row t%S (:24-33); row 0 seeds min=max=key (:35-38); later rows
+//   update channel-wise with strict '<' and '>' (:40-43), so among equal values (e.g.
+//   -0 and +0) the first-seen one is kept.  Comparisons here are fp32 compares of the
+//   exact fp16 values, written as explicit compare-and-select (fminf/__hmin do not
+//   promise the first-seen zero sign).
+#include "qk_internal.cuh"
+
+namespace qk {
+namespace {
+
+__device__ __forceinline__ size_t meta_index(size_t slice_meta, size_t s, uint32_t page,
+                                             int D, int minmax, int c) {
+    return s * slice_meta + size_t(page / kMetaTile) * 2 * D * kMetaTile +
+           size_t(minmax) * D * kMetaTile + size_t(c) * kMetaTile + (page % kMetaTile);
+}
+
+// One CTA per (sequence, KV head), one thread per channel.  Every CTA of a sequence reads
+// the same token count; the last one to finish (ticket) bumps it, so no CTA can observe
+// the new count early.
+__global__ void append_kernel(__half* __restrict__ kp, __half* __restrict__ vp,
+                              __half* __restrict__ meta, int32_t* __restrict__ len,
+                              int32_t* __restrict__ ticket, int32_t* __restrict__ status,
+                              const __half* __restrict__ k, const __half* __restrict__ v,
+                              uint32_t layer, uint32_t B, uint32_t Hkv, uint32_t S, int D,
+                              uint32_t head_dim, size_t slice_kv, size_t slice_meta,
+                              uint32_t capacity) {
+    __shared__ int last;
+    const uint32_t b = blockIdx.x, h = blockIdx.y, c = threadIdx.x;
+    const uint32_t t = static_cast<uint32_t>(len[layer * B + b]);
+    if (t >= capacity) {
+        if (c == 0) record_status(status, QK_DEV_CAPACITY);
+        return;
+    }
+    const uint32_t page = t / S, row = t % S;
+    const size_t in = (size_t(b) * Hkv + h) * head_dim + c;
+    const __half x = c < head_dim ? k[in] : __float2half(0.0f);
+    const __half y = c < head_dim ? v[in] : __float2half(0.0f);
+    const size_t s = (size_t(layer) * B + b) * Hkv + h;
+    const size_t kv = s * slice_kv + (size_t(page) * S + row) * D + c;
+    kp[kv] = x;
+    vp[kv] = y;
+    __half* mn = meta + meta_index(slice_meta, s, page, D, 0, c);
+    __half* mx = meta + meta_index(slice_meta, s, page, D, 1, c);
+    if (row == 0) {
+        *mn = x;
+        *mx = x;
+    } else {
+        const float xf = __half2float(x);
+        if (xf < __half2float(*mn)) *mn = x;
+        if (xf > __half2float(*mx)) *mx = x;
+    }
+    __syncthreads();
+    if (c == 0) last = (atomicAdd(ticket + layer * B + b, 1) == int(Hkv) - 1);
+    __syncthreads();
+    if (last && c == 0) {
+        ticket[layer * B + b] = 0;
+        len[layer * B + b] = int32_t(t + 1);
+    }
+}
+
+// Bulk prefill of n tokens starting at token t0 of one sequence: one CTA per (page,
+// KV head), one thread per channel.  Each thread walks its page's new rows in token
+// order with the same strict compares as append, continuing from the stored metadata
+// when the first page is already partly filled, so the result is bitwise the
+// metadata n single appends would leave.
+__global__ void prefill_kernel(__half* __restrict__ kp, __half* __restrict__ vp,
+                               __half* __restrict__ meta, int32_t* __restrict__ len,
+                               const __half* __restrict__ k, const __half* __restrict__ v,
+                               uint32_t layer, uint32_t seq, uint32_t B, uint32_t Hkv,
+                               uint32_t S, int D, uint32_t head_dim, size_t slice_kv,
+                               size_t slice_meta, uint32_t t0, uint32_t n) {
+    const uint32_t page = t0 / S + blockIdx.x;
+    const uint32_t h = blockIdx.y;
+    const uint32_t c = threadIdx.x;
+    const size_t s = (size_t(layer) * B + seq) * Hkv + h;
+    const uint32_t r_begin = (blockIdx.x == 0) ? t0 % S : 0;
+    const uint32_t page_end = page * S + S;
+    const uint32_t r_end = (t0 + n < page_end) ? (t0 + n - page * S) : S;
+    __half mn = __float2half(0.0f), mx = __float2half(0.0f);
+    __half* mnp = meta + meta_index(slice_meta, s, page, D, 0, c);
+    __half* mxp = meta + meta_index(slice_meta, s, page, D, 1, c);
+    if (r_begin != 0) {
+        mn = *mnp;
+        mx = *mxp;
+    }
+    for (uint32_t r = r_begin; r < r_end; ++r) {
+        const uint32_t i = page * S + r - t0;  // index among the new tokens
+        const size_t in = (size_t(h) * n + i) * head_dim + c;
+        const __half x = c < head_dim ? k[in] : __float2half(0.0f);
+        const __half y = c < head_dim ? v[in] : __float2half(0.0f);
+        const size_t kv = s * slice_kv + (size_t(page) * S + r) * D + c;
+        kp[kv] = x;
+        vp[kv] = y;
+        if (r == 0) {
+            mn = x;
+            mx = x;
+        } else {
+            const float xf = __half2float(x);
+            if (xf < __half2float(mn)) mn = x;
+            if (xf > __half2float(mx)) mx = x;
+        }
+    }
+    *mnp = mn;
+    *mxp = mx;
+    if (blockIdx.x == 0 && blockIdx.y == 0 && c == 0) len[layer * B + seq] = int32_t(t0 + n);
+}
+
+}  // namespace
+
+int launch_append(qk_cache* c, uint32_t layer, const __half* k, const __half* v,
+                  uint32_t batch, cudaStream_t st) {
+    append_kernel<<<dim3(batch, c->Hkv), c->D, 0, st>>>(
+        c->k_pool, c->v_pool, c->meta, c->d_len, c->len_ticket, c->d_status, k, v, layer, c->B,
+        c->Hkv, c->S, c->D, c->desc.head_dim, c->slice_kv, c->slice_meta, c->desc.max_tokens);
+    c->launches++;
+    return cuda_check(cudaGetLastError(), "append_kernel");
+}
+
+int launch_prefill(qk_cache* c, uint32_t layer, uint32_t seq, const __half* k,
+                   const __half* v, uint32_t n, uint32_t t0, cudaStream_t st) {
+    const uint32_t pages = (t0 + n - 1) / c->S - t0 / c->S + 1;
+    prefill_kernel<<<dim3(pages, c->Hkv), c->D, 0, st>>>(
+        c->k_pool, c->v_pool, c->meta, c->d_len, k, v, layer, seq, c->B, c->Hkv, c->S, c->D,
+        c->desc.head_dim, c->slice_kv, c->slice_meta, t0, n);
+    c->launches++;
+    return cuda_check(cudaGetLastError(), "prefill_kernel");
+}
+
+}  // namespace qk

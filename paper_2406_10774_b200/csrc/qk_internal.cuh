@@ -1,0 +1,138 @@
+// qk_internal.cuh -- shared state and helpers of the B200 Quest decode library.
+//
+// Device layout (all fp16 unless noted), per cache slice s = (layer * max_batch + seq) *
+// num_kv_heads + kv_head, D = head_dim padded up to 64/128/256 with zero channels:
+//   K pool   k_pool[s][Pmax][S][D]           one page = S*D*2 contiguous bytes (4 KiB at
+//   V pool   v_pool[s][Pmax][S][D]           S=16, D=128), the unit of a page fetch
+//   metadata meta[s][Pmax/64][2][D][64]       channel-major tiles of 64 pages: row
+//                                            (tile, minmax, c) holds channel c of 64
+//                                            consecutive pages (128 contiguous bytes), so
+//                                            the estimate kernel reads, per channel, only
+//                                            the row the query's sign selects
+//   lengths  len[layer][seq]                 int32 token counts (device copy; the host
+//                                            keeps a shadow for validation / grid sizing)
+// Zero padding channels never change a result: padded q is 0, so every estimate term
+// and every logit term they add is +-0.
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <string>
+#include <vector>
+
+#include "questkv_b200.h"
+
+namespace qk {
+
+constexpr int kMetaTile = 64;       // pages per metadata tile
+constexpr int kMaxSplits = 64;      // split-KV partitions per (sequence, query head)
+constexpr int kMinPagesPerSplit = 8;
+constexpr uint32_t kMaxPages = 16384;  // top-K keeps one slice's scores in shared memory
+
+struct Status {
+    int code = QK_OK;
+    std::string msg;
+};
+
+int set_error(int code, const std::string& msg);
+int cuda_check(cudaError_t err, const char* what);
+
+}  // namespace qk
+
+struct qk_cache {
+    qk_cache_desc desc{};
+    int D = 0;               // padded head dim
+    uint32_t S = 0, L = 0, B = 0, Hq = 0, Hkv = 0, G = 0;
+    uint32_t Pmax = 0;       // logical pages per slice
+    uint32_t Ptiles = 0;     // metadata tiles per slice
+    size_t slice_kv = 0;     // halves per slice in k_pool / v_pool
+    size_t slice_meta = 0;   // halves per slice in meta
+    __half* k_pool = nullptr;
+    __half* v_pool = nullptr;
+    __half* meta = nullptr;
+    int32_t* d_len = nullptr;            // [L][B]
+    std::vector<uint32_t> h_len;         // host shadow [L][B]
+    float* ws_partial = nullptr;         // [B][Hq][kMaxSplits][D + 2]
+    int32_t* ws_ticket = nullptr;        // [B][Hq]
+    int32_t* d_status = nullptr;         // first device-side error code
+    int32_t* len_ticket = nullptr;       // [L][B] CTAs done with this step's length
+    double* ws_scores = nullptr;         // [B][Hq][Pmax]  (fused step)
+    int32_t* ws_pages = nullptr;         // [B][Hq][Pmax]
+    int32_t* ws_counts = nullptr;        // [B][Hq]
+    uint16_t* ws_io = nullptr;           // staging for qk_decode_step_host
+    float* ws_out = nullptr;             // [B][Hq][head_dim] fp32
+    unsigned long long* probe = nullptr; // phase timestamps of the fused kernel (QK_PROBE)
+    uint64_t device_bytes = 0;
+    std::atomic<uint64_t> launches{0};
+
+    size_t slice(uint32_t layer, uint32_t seq, uint32_t h) const {
+        return (size_t(layer) * B + seq) * Hkv + h;
+    }
+};
+
+// Device-side error codes recorded in qk_cache::d_status.
+enum : int32_t {
+    QK_DEV_OK = 0,
+    QK_DEV_PAGE_OUT_OF_RANGE = 1,
+    QK_DEV_PAGE_NOT_ASCENDING = 2,
+    QK_DEV_EMPTY_SELECTION = 3,
+    QK_DEV_CAPACITY = 4,
+};
+
+// Kernel launchers (one translation unit each).
+namespace qk {
+int launch_append(qk_cache* c, uint32_t layer, const __half* k, const __half* v,
+                  uint32_t batch, cudaStream_t st);
+int launch_prefill(qk_cache* c, uint32_t layer, uint32_t seq, const __half* k,
+                   const __half* v, uint32_t n, uint32_t t0, cudaStream_t st);
+int launch_estimate(const qk_cache* c, uint32_t layer, const __half* q, uint32_t batch,
+                    double* scores, uint32_t stride, uint32_t max_pages, cudaStream_t st);
+int launch_topk(const qk_cache* c, uint32_t layer, const double* scores, uint32_t sstride,
+                uint32_t batch, const qk_selection_cfg& cfg, int32_t* pages,
+                uint32_t pstride, int32_t* counts, uint32_t max_pages, cudaStream_t st);
+int launch_attend(const qk_cache* c, uint32_t layer, const __half* q, uint32_t batch,
+                  const int32_t* pages, uint32_t pstride, const int32_t* counts,
+                  bool dense, uint32_t max_list, void* out, int out_dtype, float* lse,
+                  cudaStream_t st);
+int launch_decode(qk_cache* c, uint32_t layer, const __half* q, const __half* k,
+                  const __half* v, uint32_t batch, const qk_selection_cfg& cfg,
+                  uint32_t max_pages_after, void* out, int out_dtype, int32_t* pages,
+                  uint32_t pstride, int32_t* counts, cudaStream_t st);
+}  // namespace qk
+
+// ---- device helpers ------------------------------------------------------------------
+
+namespace qk {
+
+__device__ __forceinline__ void record_status(int32_t* status, int32_t code) {
+    atomicCAS(status, QK_DEV_OK, code);
+}
+
+// Ordered unsigned key of a double: larger double <-> larger key (no NaNs expected).
+__device__ __forceinline__ unsigned long long order_key(double x) {
+    unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(x));
+    return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+
+__device__ __forceinline__ int4 ld_nc_v4(const void* p) {
+    int4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N));
+}
+
+}  // namespace qk

@@ -1,0 +1,195 @@
+"""GPU parity of the fused decode step (qk_decode_step, one kernel per layer step):
+append -> estimate -> top-K -> sparse attend, against the oracle run per query head on its
+KV head's cache.  Scores are not exposed by the fused kernel, so selection (bitwise) and
+outputs (relative L2 <= 1e-5) are checked, across MHA/GQA, cluster sizes (1..8 CTAs per
+KV head), ragged batches, selection modes and multi-step appends, plus CUDA-graph replay."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import half
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def qk():
+    from paper_2406_10774_b200 import questkv
+
+    return questkv
+
+
+def rel_l2(got, want):
+    got, want = np.asarray(got, np.float64), np.asarray(want, np.float64)
+    return np.linalg.norm(got - want) / (np.linalg.norm(want) + 1e-30)
+
+
+class Layer:
+    """A QuestCache layer plus a host mirror of every slice for the oracle."""
+
+    def __init__(self, qk, rng, B, Hq, Hkv, d, S, lens, extra=16):
+        self.qc = qk.QuestCache(d, S, max_batch=B, num_q_heads=Hq, num_kv_heads=Hkv,
+                                max_tokens=max(lens) + extra)
+        self.B, self.Hq, self.Hkv, self.d, self.S = B, Hq, Hkv, d, S
+        self.keys, self.vals = [], []
+        sd = 1 / np.sqrt(d)
+        for b, L in enumerate(lens):
+            k = half(rng.standard_normal((Hkv, L, d)) * sd)
+            v = half(rng.standard_normal((Hkv, L, d)) * sd)
+            if L:
+                self.qc.prefill(0, b, torch.from_numpy(k).half().cuda(),
+                                torch.from_numpy(v).half().cuda())
+            self.keys.append(k)
+            self.vals.append(v)
+
+    def step(self, rng, budget, force=True, enabled=True, append=True):
+        B, Hq, Hkv, d = self.B, self.Hq, self.Hkv, self.d
+        sd = 1 / np.sqrt(d)
+        q = half(rng.standard_normal((B, Hq, d)) * sd)
+        kn = half(rng.standard_normal((B, Hkv, d)) * sd)
+        vn = half(rng.standard_normal((B, Hkv, d)) * sd)
+        if append:
+            for b in range(B):
+                self.keys[b] = np.concatenate([self.keys[b], kn[b][:, None]], axis=1)
+                self.vals[b] = np.concatenate([self.vals[b], vn[b][:, None]], axis=1)
+        P = max(k.shape[1] for k in self.keys) // self.S + 1
+        pages = torch.full((B, Hq, P), -1, dtype=torch.int32, device="cuda")
+        counts = torch.zeros((B, Hq), dtype=torch.int32, device="cuda")
+        t = lambda a: torch.from_numpy(a).half().cuda()  # noqa: E731
+        out = self.qc.decode_step(0, t(q), t(kn) if append else None, t(vn) if append else None,
+                                  budget, force, enabled, pages=pages, counts=counts)
+        self.qc.check_status()
+        return q, out.cpu().numpy(), pages.cpu().numpy(), counts.cpu().numpy()
+
+    def check(self, oracle_c, q, out, pages, counts, budget, force=True, enabled=True):
+        G = self.Hq // self.Hkv
+        for b in range(self.B):
+            for h in range(self.Hq):
+                k, v = self.keys[b][h // G], self.vals[b][h // G]
+                s_want, p_want, o_want = oracle_c.quest_step(q[b, h], k, v, self.S, budget,
+                                                             force, enabled)
+                s_got = self.qc.step_scores(b, h, len(s_want))
+                assert np.array_equal(s_got.view(np.uint64), s_want.view(np.uint64)), (b, h)
+                got = pages[b, h, : counts[b, h]].tolist()
+                assert got == p_want.tolist(), (b, h)
+                assert rel_l2(out[b, h], o_want) <= TOL, (b, h)
+
+
+@pytest.mark.parametrize("B,Hq,Hkv,d,lens,budget", [
+    (1, 8, 8, 128, [32767], 2048),        # cfg2 length, the newest token opens page 2047
+    (1, 32, 32, 128, [8191], 1024),       # cfg1 (Llama-2-7B layer, 8K, budget 1024)
+    (3, 8, 2, 128, [5000, 100, 1], 512),  # GQA 4, ragged, a 1-token sequence
+    (2, 16, 2, 128, [3001, 2047], 256),   # GQA 8
+    (2, 4, 2, 64, [1500, 33], 128),       # head_dim 64, GQA 2
+    (1, 2, 2, 128, [40000], 4096),        # long context, cluster of 8, K = 256
+    (1, 4, 4, 100, [700], 64),            # padded head_dim
+])
+def test_fused_step_vs_oracle(qk, oracle_c, B, Hq, Hkv, d, lens, budget):
+    rng = np.random.default_rng(sum(lens) + 7 * Hq + d)
+    layer = Layer(qk, rng, B, Hq, Hkv, d, 16, lens)
+    q, out, pages, counts = layer.step(rng, budget)
+    layer.check(oracle_c, q, out, pages, counts, budget)
+
+
+@pytest.mark.parametrize("budget,force,enabled", [
+    (16, True, True),      # K = 1: only the newest page
+    (16, False, True),     # K = 1 by score
+    (512, False, True),    # no forced page
+    (512, True, False),    # selection disabled: dense over every page
+    (1 << 20, True, True),  # budget covers the cache
+])
+def test_fused_selection_modes(qk, oracle_c, budget, force, enabled):
+    rng = np.random.default_rng(budget + force)
+    layer = Layer(qk, rng, 2, 4, 4, 128, 16, [2500, 97])
+    q, out, pages, counts = layer.step(rng, budget, force, enabled)
+    layer.check(oracle_c, q, out, pages, counts, budget, force, enabled)
+
+
+def test_fused_multi_step_appends(qk, oracle_c):
+    """Five consecutive steps: every KV head of every sequence appends once per step (the
+    length is bumped once, after all heads read it), pages open at the boundary."""
+    rng = np.random.default_rng(77)
+    layer = Layer(qk, rng, 2, 8, 4, 128, 16, [62, 1023])
+    for step in range(5):
+        q, out, pages, counts = layer.step(rng, 256)
+        layer.check(oracle_c, q, out, pages, counts, 256)
+        assert layer.qc.token_count(0, 0) == 63 + step
+        assert layer.qc.token_count(0, 1) == 1024 + step
+        for b in range(2):
+            mn, mx = layer.qc.read_metadata(0, b, 3)
+            omn, omx = oracle_c.metadata(layer.keys[b][3], 16)
+            assert np.array_equal(mn.astype(np.float32), omn)
+            assert np.array_equal(mx.astype(np.float32), omx)
+
+
+@pytest.mark.parametrize("G", [1, 4])
+def test_fused_scores_adversarial_values(qk, oracle_c, G):
+    """Exactness of the fused estimate's fp16 -> f64 conversions (XU F2F on even channels,
+    the integer 2^-1008-scaled path on odd ones): keys and queries drawn from fp16
+    subnormals, +-0, the extremes +-65504 and ordinary values, mixed signs -- scores
+    bitwise equal to the oracle."""
+    rng = np.random.default_rng(31 + G)
+    specials = np.array([0.0, -0.0, 2 ** -24, -(2 ** -24), 3 * 2 ** -24, -(1023 * 2 ** -24),
+                         2 ** -14, -(2 ** -14), 65504.0, -65504.0, 1.0, -1.0, 0.5, -3.25],
+                        np.float32)
+    Hkv, d, S, L = 2, 128, 16, 1000
+    qc = qk.QuestCache(d, S, num_q_heads=Hkv * G, num_kv_heads=Hkv, max_tokens=L + 1)
+    keys = half(rng.standard_normal((Hkv, L, d)))
+    mask = rng.random(keys.shape) < 0.3
+    keys[mask] = rng.choice(specials, size=mask.sum())
+    vals = half(rng.standard_normal((Hkv, L, d)) * 0.1)
+    qc.prefill(0, 0, torch.from_numpy(keys).half().cuda(), torch.from_numpy(vals).half().cuda())
+    q = half(rng.standard_normal((1, Hkv * G, d)) * 1e-3)
+    qmask = rng.random(q.shape) < 0.3
+    q[qmask] = rng.choice(specials[:8], size=qmask.sum())  # keep products finite
+    out = qc.decode_step(0, torch.from_numpy(q).half().cuda(), None, None, 256)
+    qc.check_status()
+    for h in range(Hkv * G):
+        mn, mx = oracle_c.metadata(keys[h // G], S)
+        want = oracle_c.estimate_all(q[0, h], mn, mx)
+        got = qc.step_scores(0, h, len(want))
+        assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), h
+    assert torch.isfinite(out).all()
+
+
+def test_fused_step_without_append(qk, oracle_c):
+    rng = np.random.default_rng(5)
+    layer = Layer(qk, rng, 1, 4, 4, 128, 16, [4000])
+    q, out, pages, counts = layer.step(rng, 1024, append=False)
+    layer.check(oracle_c, q, out, pages, counts, 1024)
+    assert layer.qc.token_count(0, 0) == 4000
+
+
+def test_fused_step_graph_replay(qk, oracle_c):
+    """A CUDA graph of the step replayed 4 times equals 4 eager steps (device lengths
+    advance on replay; qk_sync_lengths refreshes the host shadow)."""
+    rng = np.random.default_rng(9)
+    B, H, d, S, L = 1, 8, 128, 16, 3000
+    eager = Layer(qk, np.random.default_rng(1), B, H, H, d, S, [L])
+    graphed = Layer(qk, np.random.default_rng(1), B, H, H, d, S, [L])
+    qs = [torch.from_numpy(half(rng.standard_normal((B, H, d)) / np.sqrt(d))).half().cuda()
+          for _ in range(4)]
+    ks = [torch.from_numpy(half(rng.standard_normal((B, H, d)) / np.sqrt(d))).half().cuda()
+          for _ in range(4)]
+    qb, kb, vb = qs[0].clone(), ks[0].clone(), ks[0].clone()
+    out_g = torch.zeros((B, H, d), dtype=torch.float32, device="cuda")
+    s = torch.cuda.Stream()
+    warm = Layer(qk, np.random.default_rng(2), B, H, H, d, S, [16])
+    warm.qc.decode_step(0, qb, kb, vb, 512, stream=s)  # load the kernel before capture
+    s.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        graphed.qc.decode_step(0, qb, kb, vb, 512, out=out_g, stream=s)
+    for i in range(4):
+        with torch.cuda.stream(s):
+            qb.copy_(qs[i])
+            kb.copy_(ks[i])
+            vb.copy_(ks[i])
+            g.replay()
+        s.synchronize()
+        ref = eager.qc.decode_step(0, qs[i], ks[i], ks[i], 512)
+        assert torch.equal(out_g, ref), i
+    graphed.qc.sync_lengths()
+    assert graphed.qc.token_count(0, 0) == L + 4 == eager.qc.token_count(0, 0)
