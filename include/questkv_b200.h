@@ -190,6 +190,38 @@ QK_API int qk_decode_step_host(qk_cache *cache, uint32_t layer, const uint16_t *
                         const uint16_t *k_host, const uint16_t *v_host, uint32_t batch,
                         const qk_selection_cfg *cfg, float *out_host, void *stream);
 
+/* Host-buffer forms of the entry points above, for callers that keep activations on the
+ * host (the questkv:: C++ layer in questkv_b200.hpp binds these).  Each stages its
+ * inputs through the cache's device workspaces, runs the device entry point on `stream`
+ * and copies the result back; all are synchronous and return the same statuses.
+ * Arrays have the device forms' layouts; outputs are f32 (out) / f64 (scores). */
+QK_API int qk_append_host(qk_cache *cache, uint32_t layer, const uint16_t *k_host,
+                          const uint16_t *v_host, uint32_t batch, void *stream);
+QK_API int qk_prefill_host(qk_cache *cache, uint32_t layer, uint32_t seq, const uint16_t *k_host,
+                           const uint16_t *v_host, uint32_t n_tokens, void *stream);
+QK_API int qk_estimate_host(const qk_cache *cache, uint32_t layer, const uint16_t *q_host,
+                            uint32_t batch, double *scores_host, uint32_t scores_stride,
+                            void *stream);
+QK_API int qk_select_topk_host(const qk_cache *cache, uint32_t layer, const double *scores_host,
+                               uint32_t scores_stride, uint32_t batch,
+                               const qk_selection_cfg *cfg, int32_t *pages_host,
+                               uint32_t pages_stride, int32_t *counts_host, void *stream);
+/* Page lists are validated on the host first, with sparse_attention's errors
+ * (attention.cpp:99-106): empty -> INVALID_ARGUMENT, out of range -> OUT_OF_RANGE,
+ * duplicate / not ascending -> INVALID_ARGUMENT. */
+QK_API int qk_sparse_attend_host(const qk_cache *cache, uint32_t layer, const uint16_t *q_host,
+                                 uint32_t batch, const int32_t *pages_host,
+                                 uint32_t pages_stride, const int32_t *counts_host,
+                                 float *out_host, float *lse_host, void *stream);
+QK_API int qk_dense_attend_host(const qk_cache *cache, uint32_t layer, const uint16_t *q_host,
+                                uint32_t batch, float *out_host, float *lse_host, void *stream);
+
+/* Diagnostics / parity: with `on`, qk_decode_step estimates every page (also the forced
+ * newest page, and when the budget covers the cache) and keeps the scores for
+ * qk_debug_step_scores.  Off by default: the fused step then skips scores selection
+ * cannot use. */
+QK_API int qk_debug_keep_scores(qk_cache *cache, int32_t on);
+
 /* Re-reads the device token counts into the host-side shadow (synchronous).  Needed
  * after replaying a captured CUDA graph of qk_decode_step, whose appends advance only the
  * device counts. */
@@ -200,9 +232,9 @@ QK_API int qk_sync_lengths(qk_cache *cache, void *stream);
 QK_API int qk_check_status(qk_cache *cache, void *stream);
 
 /* Diagnostics: with QK_PROBE=1 in the environment at qk_cache_create, the fused decode
- * kernel records 8 %globaltimer stamps per CTA (entry, after griddepcontrol.wait, end of
- * estimate, after the first cluster barrier, after selection, end of attention, after
- * the second barrier, exit).  Copies the first n (synchronous). */
+ * kernel records up to 32 %globaltimer stamps per CTA at its phase boundaries (see
+ * decode.cu; tools/probe_fused.py prints the timeline).  Copies the first n and clears
+ * the record (synchronous). */
 QK_API int qk_debug_probe(qk_cache *cache, uint64_t *host, uint32_t n, void *stream);
 
 /* Diagnostics: the page scores the last qk_decode_step computed for (seq, q_head), pages

@@ -85,6 +85,16 @@ SIGNATURES = {
     "qk_debug_probe": (ctypes.c_int, [_P, _P, _U32, _P]),
     "qk_debug_step_scores": (ctypes.c_int, [_P, _U32, _U32, _P, _U32, _P]),
     "qk_kernel_launches": (ctypes.c_uint64, [_P]),
+    "qk_debug_keep_scores": (ctypes.c_int, [_P, _I32]),
+    "qk_append_host": (ctypes.c_int, [_P, _U32, _P, _P, _U32, _P]),
+    "qk_prefill_host": (ctypes.c_int, [_P, _U32, _U32, _P, _P, _U32, _P]),
+    "qk_estimate_host": (ctypes.c_int, [_P, _U32, _P, _U32, _P, _U32, _P]),
+    "qk_select_topk_host": (
+        ctypes.c_int,
+        [_P, _U32, _P, _U32, _U32, ctypes.POINTER(qk_selection_cfg), _P, _U32, _P, _P],
+    ),
+    "qk_sparse_attend_host": (ctypes.c_int, [_P, _U32, _P, _U32, _P, _U32, _P, _P, _P, _P]),
+    "qk_dense_attend_host": (ctypes.c_int, [_P, _U32, _P, _U32, _P, _P, _P]),
 }
 
 _lib = None

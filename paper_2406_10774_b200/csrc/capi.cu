@@ -79,7 +79,8 @@ int dmalloc(qk_cache* c, T** p, size_t count) {
 void free_cache(qk_cache* c) {
     void* ptrs[] = {c->k_pool,    c->v_pool,    c->meta,      c->d_len,     c->ws_partial,
                     c->ws_ticket, c->d_status,  c->ws_scores, c->ws_pages,  c->ws_counts,
-                    c->ws_io,     c->ws_out,    c->len_ticket, c->probe};
+                    c->ws_io,     c->ws_out,    c->len_ticket, c->probe,     c->ws_lse,
+                    c->prange};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     delete c;
@@ -142,26 +143,28 @@ int qk_cache_create(const qk_cache_desc* desc, qk_cache** out) {
     c->Hkv = desc->num_kv_heads;
     c->G = G;
     c->Pmax = uint32_t(pmax);
-    c->Ptiles = (c->Pmax + kMetaTile - 1) / kMetaTile;
+    c->Mrow = (c->Pmax + kMetaAlign - 1) / kMetaAlign * kMetaAlign;
     c->slice_kv = size_t(c->Pmax) * c->S * c->D;
-    c->slice_meta = size_t(c->Ptiles) * 2 * c->D * kMetaTile;
+    c->slice_meta = size_t(2) * c->D * c->Mrow;
     const size_t slices = size_t(c->L) * c->B * c->Hkv;
     c->h_len.assign(size_t(c->L) * c->B, 0);
     int rc = QK_OK;
     if (!rc) rc = dmalloc(c, &c->k_pool, slices * c->slice_kv);
     if (!rc) rc = dmalloc(c, &c->v_pool, slices * c->slice_kv);
     if (!rc) rc = dmalloc(c, &c->meta, slices * c->slice_meta);
+    if (!rc) rc = dmalloc(c, &c->prange, slices * c->Mrow);
     if (!rc) rc = dmalloc(c, &c->d_len, size_t(c->L) * c->B);
     if (!rc) rc = dmalloc(c, &c->ws_partial, size_t(c->B) * c->Hq * kMaxSplits * (c->D + 2));
     if (!rc) rc = dmalloc(c, &c->ws_ticket, size_t(c->B) * c->Hq);
     if (!rc) rc = dmalloc(c, &c->d_status, 1);
     if (!rc) rc = dmalloc(c, &c->len_ticket, size_t(c->L) * c->B);
-    if (!rc && getenv("QK_PROBE")) rc = dmalloc(c, &c->probe, size_t(c->B) * c->Hkv * 8 * 16);
+    if (!rc && getenv("QK_PROBE")) rc = dmalloc(c, &c->probe, size_t(c->B) * c->Hkv * kMaxClusterCtas * kProbeSlots);
     if (!rc) rc = dmalloc(c, &c->ws_scores, size_t(c->B) * c->Hq * c->Pmax);
     if (!rc) rc = dmalloc(c, &c->ws_pages, size_t(c->B) * c->Hq * c->Pmax);
     if (!rc) rc = dmalloc(c, &c->ws_counts, size_t(c->B) * c->Hq);
     if (!rc) rc = dmalloc(c, &c->ws_io, size_t(c->B) * (c->Hq + 2 * c->Hkv) * desc->head_dim);
     if (!rc) rc = dmalloc(c, &c->ws_out, size_t(c->B) * c->Hq * desc->head_dim);
+    if (!rc) rc = dmalloc(c, &c->ws_lse, size_t(c->B) * c->Hq);
     if (!rc) rc = cuda_check(cudaDeviceSynchronize(), "qk_cache_create");
     if (rc) {
         free_cache(c);
@@ -260,15 +263,14 @@ namespace qk {
 namespace readback {
 
 __global__ void gather_meta_kernel(const __half* __restrict__ meta, __half* __restrict__ mn,
-                                   __half* __restrict__ mx, size_t base, uint32_t page0,
-                                   uint32_t n, int D, uint32_t head_dim) {
+                                   __half* __restrict__ mx, size_t slice_meta, uint32_t mrow,
+                                   size_t s, uint32_t page0, uint32_t n, int D,
+                                   uint32_t head_dim) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n * head_dim) return;
     const uint32_t p = page0 + i / head_dim, ch = i % head_dim;
-    const size_t off = base + size_t(p / kMetaTile) * 2 * D * kMetaTile + size_t(ch) * kMetaTile +
-                       (p % kMetaTile);
-    mn[i] = meta[off];
-    mx[i] = meta[off + size_t(D) * kMetaTile];
+    mn[i] = meta[meta_offset(slice_meta, mrow, s, p, D, 0, int(ch))];
+    mx[i] = meta[meta_offset(slice_meta, mrow, s, p, D, 1, int(ch))];
 }
 
 __global__ void gather_kv_kernel(const __half* __restrict__ kp, const __half* __restrict__ vp,
@@ -318,8 +320,8 @@ int qk_read_metadata(const qk_cache* cc, uint32_t layer, uint32_t seq, uint32_t 
     int rc = cuda_check(cudaMalloc(&tmp, 2 * n * sizeof(__half)), "qk_read_metadata");
     if (rc) return rc;
     gather_meta_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(
-        c->meta, tmp, tmp + n, c->slice(layer, seq, kv_head) * c->slice_meta, page0, n_pages,
-        c->D, c->desc.head_dim);
+        c->meta, tmp, tmp + n, c->slice_meta, c->Mrow, c->slice(layer, seq, kv_head), page0,
+        n_pages, c->D, c->desc.head_dim);
     c->launches++;
     rc = cuda_check(cudaGetLastError(), "gather_meta_kernel");
     if (!rc) rc = read_back(c, tmp, tmp + n, min_host, max_host, n, st);
@@ -463,7 +465,7 @@ int qk_decode_step(qk_cache* c, uint32_t layer, const uint16_t* q, const uint16_
     DeviceGuard guard(c->desc.device);
     const int rc = launch_decode(c, layer, reinterpret_cast<const __half*>(q),
                                  reinterpret_cast<const __half*>(k),
-                                 reinterpret_cast<const __half*>(v), batch, *cfg, c->Pmax, out,
+                                 reinterpret_cast<const __half*>(v), batch, *cfg, mp, out,
                                  out_dtype, pages_out, pages_stride, counts_out,
                                  as_stream(stream));
     if (rc) return rc;
@@ -503,14 +505,184 @@ int qk_decode_step_host(qk_cache* c, uint32_t layer, const uint16_t* q_host,
     return rc;
 }
 
+// ---- host-buffer variants (the questkv:: C++ layer, include/questkv_b200.hpp) ----------
+// Each stages its inputs into the cache's device workspaces, runs the device entry point
+// on `stream` and copies the result back; synchronous.
+
+int qk_append_host(qk_cache* c, uint32_t layer, const uint16_t* k_host, const uint16_t* v_host,
+                   uint32_t batch, void* stream) {
+    if (!c || !k_host || !v_host)
+        return set_error(QK_ERR_INVALID_ARGUMENT, "KvCache::append: null argument");
+    if (int rc = check_layer_batch(c, layer, batch, "KvCache::append")) return rc;
+    DeviceGuard guard(c->desc.device);
+    cudaStream_t st = as_stream(stream);
+    const size_t nkv = size_t(batch) * c->Hkv * c->desc.head_dim;
+    uint16_t* dk = c->ws_io;
+    uint16_t* dv = dk + nkv;
+    int rc = cuda_check(cudaMemcpyAsync(dk, k_host, nkv * 2, cudaMemcpyHostToDevice, st), "h2d k");
+    if (!rc) rc = cuda_check(cudaMemcpyAsync(dv, v_host, nkv * 2, cudaMemcpyHostToDevice, st), "h2d v");
+    if (!rc) rc = qk_append(c, layer, dk, dv, batch, stream);
+    if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "qk_append_host");
+    return rc;
+}
+
+int qk_prefill_host(qk_cache* c, uint32_t layer, uint32_t seq, const uint16_t* k_host,
+                    const uint16_t* v_host, uint32_t n_tokens, void* stream) {
+    if (!c || !k_host || !v_host)
+        return set_error(QK_ERR_INVALID_ARGUMENT, "qk_prefill: null argument");
+    if (n_tokens == 0) return QK_OK;
+    DeviceGuard guard(c->desc.device);
+    cudaStream_t st = as_stream(stream);
+    const size_t n = size_t(c->Hkv) * n_tokens * c->desc.head_dim;
+    uint16_t* tmp = nullptr;
+    int rc = cuda_check(cudaMalloc(&tmp, 2 * n * sizeof(uint16_t)), "qk_prefill_host");
+    if (rc) return rc;
+    rc = cuda_check(cudaMemcpyAsync(tmp, k_host, n * 2, cudaMemcpyHostToDevice, st), "h2d k");
+    if (!rc) rc = cuda_check(cudaMemcpyAsync(tmp + n, v_host, n * 2, cudaMemcpyHostToDevice, st), "h2d v");
+    if (!rc) rc = qk_prefill(c, layer, seq, tmp, tmp + n, n_tokens, stream);
+    const int rs = cuda_check(cudaStreamSynchronize(st), "qk_prefill_host");
+    cudaFree(tmp);
+    return rc ? rc : rs;
+}
+
+int qk_estimate_host(const qk_cache* cc, uint32_t layer, const uint16_t* q_host, uint32_t batch,
+                     double* scores_host, uint32_t scores_stride, void* stream) {
+    qk_cache* c = const_cast<qk_cache*>(cc);
+    if (!c || !q_host || !scores_host)
+        return set_error(QK_ERR_INVALID_ARGUMENT, "estimate_all: null argument");
+    if (int rc = check_layer_batch(c, layer, batch, "estimate_all")) return rc;
+    if (scores_stride > c->Pmax)
+        return set_error(QK_ERR_INVALID_ARGUMENT, "estimate_all: scores_stride above max_pages");
+    DeviceGuard guard(c->desc.device);
+    cudaStream_t st = as_stream(stream);
+    const size_t nq = size_t(batch) * c->Hq * c->desc.head_dim;
+    int rc = cuda_check(cudaMemcpyAsync(c->ws_io, q_host, nq * 2, cudaMemcpyHostToDevice, st), "h2d q");
+    if (!rc) rc = qk_estimate(c, layer, c->ws_io, batch, c->ws_scores, c->Pmax, stream);
+    if (!rc && scores_stride > 0)
+        rc = cuda_check(cudaMemcpy2DAsync(scores_host, size_t(scores_stride) * 8, c->ws_scores,
+                                          size_t(c->Pmax) * 8, size_t(scores_stride) * 8,
+                                          size_t(batch) * c->Hq, cudaMemcpyDeviceToHost, st),
+                        "d2h scores");
+    if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "qk_estimate_host");
+    return rc;
+}
+
+int qk_select_topk_host(const qk_cache* cc, uint32_t layer, const double* scores_host,
+                        uint32_t scores_stride, uint32_t batch, const qk_selection_cfg* cfg,
+                        int32_t* pages_host, uint32_t pages_stride, int32_t* counts_host,
+                        void* stream) {
+    qk_cache* c = const_cast<qk_cache*>(cc);
+    if (!c || !scores_host || !cfg || !pages_host || !counts_host)
+        return set_error(QK_ERR_INVALID_ARGUMENT, "select_top_k: null argument");
+    if (int rc = check_layer_batch(c, layer, batch, "select_top_k")) return rc;
+    if (scores_stride > c->Pmax || pages_stride > c->Pmax)
+        return set_error(QK_ERR_INVALID_ARGUMENT, "select_top_k: stride above max_pages");
+    DeviceGuard guard(c->desc.device);
+    cudaStream_t st = as_stream(stream);
+    const size_t rows = size_t(batch) * c->Hq;
+    int rc = QK_OK;
+    if (scores_stride > 0)
+        rc = cuda_check(cudaMemcpy2DAsync(c->ws_scores, size_t(c->Pmax) * 8, scores_host,
+                                          size_t(scores_stride) * 8, size_t(scores_stride) * 8, rows,
+                                          cudaMemcpyHostToDevice, st),
+                        "h2d scores");
+    if (!rc)
+        rc = qk_select_topk(c, layer, c->ws_scores, c->Pmax, batch, cfg, c->ws_pages, c->Pmax,
+                            c->ws_counts, stream);
+    if (!rc && pages_stride > 0)
+        rc = cuda_check(cudaMemcpy2DAsync(pages_host, size_t(pages_stride) * 4, c->ws_pages,
+                                          size_t(c->Pmax) * 4, size_t(pages_stride) * 4, rows,
+                                          cudaMemcpyDeviceToHost, st),
+                        "d2h pages");
+    if (!rc)
+        rc = cuda_check(cudaMemcpyAsync(counts_host, c->ws_counts, rows * 4, cudaMemcpyDeviceToHost, st),
+                        "d2h counts");
+    if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "qk_select_topk_host");
+    return rc;
+}
+
+int qk_sparse_attend_host(const qk_cache* cc, uint32_t layer, const uint16_t* q_host,
+                          uint32_t batch, const int32_t* pages_host, uint32_t pages_stride,
+                          const int32_t* counts_host, float* out_host, float* lse_host,
+                          void* stream) {
+    qk_cache* c = const_cast<qk_cache*>(cc);
+    if (!c || !q_host || !pages_host || !counts_host || !out_host)
+        return set_error(QK_ERR_INVALID_ARGUMENT, "sparse_attention: null argument");
+    if (int rc = check_layer_batch(c, layer, batch, "sparse_attention")) return rc;
+    if (pages_stride == 0 || pages_stride > c->Pmax)
+        return set_error(QK_ERR_INVALID_ARGUMENT, "sparse_attention: pages_stride must be in 1..max_pages");
+    const size_t rows = size_t(batch) * c->Hq;
+    // The reference's page-list validation (attention.cpp:99-106), host side, before any
+    // device work: empty -> invalid_argument, out of range -> out_of_range, duplicates
+    // -> invalid_argument.  Lists must be given ascending (qk_sparse_attend's form).
+    for (size_t r = 0; r < rows; ++r) {
+        const uint32_t P = pages_of(c, c->h_len[size_t(layer) * c->B + r / c->Hq]);
+        const int32_t n = counts_host[r];
+        if (n <= 0) return set_error(QK_ERR_INVALID_ARGUMENT, "sparse_attention: empty page selection");
+        if (uint32_t(n) > pages_stride)
+            return set_error(QK_ERR_INVALID_ARGUMENT, "sparse_attention: count above pages_stride");
+        const int32_t* pl = pages_host + r * pages_stride;
+        for (int32_t i = 0; i < n; ++i) {
+            if (pl[i] < 0 || uint32_t(pl[i]) >= P)
+                return set_error(QK_ERR_OUT_OF_RANGE, "sparse_attention: page index out of range");
+            if (i > 0 && pl[i] <= pl[i - 1])
+                return set_error(QK_ERR_INVALID_ARGUMENT,
+                                 pl[i] == pl[i - 1] ? "sparse_attention: duplicate page index"
+                                                    : "sparse_attention: page list not ascending");
+        }
+    }
+    DeviceGuard guard(c->desc.device);
+    cudaStream_t st = as_stream(stream);
+    const size_t nq = rows * c->desc.head_dim;
+    float* dlse = lse_host ? c->ws_lse : nullptr;
+    int rc = cuda_check(cudaMemcpyAsync(c->ws_io, q_host, nq * 2, cudaMemcpyHostToDevice, st), "h2d q");
+    if (!rc)
+        rc = cuda_check(cudaMemcpy2DAsync(c->ws_pages, size_t(c->Pmax) * 4, pages_host,
+                                          size_t(pages_stride) * 4, size_t(pages_stride) * 4, rows,
+                                          cudaMemcpyHostToDevice, st),
+                        "h2d pages");
+    if (!rc) rc = cuda_check(cudaMemcpyAsync(c->ws_counts, counts_host, rows * 4, cudaMemcpyHostToDevice, st),
+                             "h2d counts");
+    if (!rc)
+        rc = qk_sparse_attend(c, layer, c->ws_io, batch, c->ws_pages, c->Pmax, c->ws_counts, c->ws_out,
+                              QK_DTYPE_F32, dlse, stream);
+    if (!rc) rc = cuda_check(cudaMemcpyAsync(out_host, c->ws_out, nq * 4, cudaMemcpyDeviceToHost, st), "d2h out");
+    if (!rc && lse_host)
+        rc = cuda_check(cudaMemcpyAsync(lse_host, dlse, rows * 4, cudaMemcpyDeviceToHost, st), "d2h lse");
+    if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "qk_sparse_attend_host");
+    if (!rc) rc = qk_check_status(c, stream);
+    return rc;
+}
+
+int qk_dense_attend_host(const qk_cache* cc, uint32_t layer, const uint16_t* q_host,
+                         uint32_t batch, float* out_host, float* lse_host, void* stream) {
+    qk_cache* c = const_cast<qk_cache*>(cc);
+    if (!c || !q_host || !out_host)
+        return set_error(QK_ERR_INVALID_ARGUMENT, "full_attention: null argument");
+    if (int rc = check_layer_batch(c, layer, batch, "full_attention")) return rc;
+    DeviceGuard guard(c->desc.device);
+    cudaStream_t st = as_stream(stream);
+    const size_t rows = size_t(batch) * c->Hq;
+    const size_t nq = rows * c->desc.head_dim;
+    float* dlse = lse_host ? c->ws_lse : nullptr;
+    int rc = cuda_check(cudaMemcpyAsync(c->ws_io, q_host, nq * 2, cudaMemcpyHostToDevice, st), "h2d q");
+    if (!rc) rc = qk_dense_attend(c, layer, c->ws_io, batch, c->ws_out, QK_DTYPE_F32, dlse, stream);
+    if (!rc) rc = cuda_check(cudaMemcpyAsync(out_host, c->ws_out, nq * 4, cudaMemcpyDeviceToHost, st), "d2h out");
+    if (!rc && lse_host)
+        rc = cuda_check(cudaMemcpyAsync(lse_host, dlse, rows * 4, cudaMemcpyDeviceToHost, st), "d2h lse");
+    if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "qk_dense_attend_host");
+    return rc;
+}
+
 int qk_debug_probe(qk_cache* c, uint64_t* host, uint32_t n, void* stream) {
     if (!c || !host) return set_error(QK_ERR_INVALID_ARGUMENT, "qk_debug_probe: null argument");
     if (!c->probe) return set_error(QK_ERR_INVALID_ARGUMENT, "qk_debug_probe: set QK_PROBE=1 before qk_cache_create");
-    const size_t cap = size_t(c->B) * c->Hkv * 8 * 16;
+    const size_t cap = size_t(c->B) * c->Hkv * kMaxClusterCtas * kProbeSlots;
     const size_t cnt = n < cap ? n : cap;
     DeviceGuard guard(c->desc.device);
     cudaStream_t st = as_stream(stream);
     int rc = cuda_check(cudaMemcpyAsync(host, c->probe, cnt * 8, cudaMemcpyDeviceToHost, st), "probe");
+    if (!rc) rc = cuda_check(cudaMemsetAsync(c->probe, 0, cap * 8, st), "probe");  // re-arm
     if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "probe");
     return rc;
 }
@@ -526,6 +698,12 @@ int qk_debug_step_scores(qk_cache* c, uint32_t seq, uint32_t q_head, double* hos
                                         size_t(n) * 8, cudaMemcpyDeviceToHost, st), "scores");
     if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "scores");
     return rc;
+}
+
+int qk_debug_keep_scores(qk_cache* c, int32_t on) {
+    if (!c) return set_error(QK_ERR_INVALID_ARGUMENT, "qk_debug_keep_scores: null cache");
+    c->keep_scores = on != 0;
+    return QK_OK;
 }
 
 int qk_sync_lengths(qk_cache* c, void* stream) {

@@ -4,32 +4,41 @@
 // (R/README.md:151-158 usage; metrics.cpp:90-95 step order; kv_store.cpp:19-47;
 //  criticality.cpp:9-81; attention.cpp:54-116).
 //
-// Work decomposition: one thread-block CLUSTER of C CTAs per (sequence, KV head) unit.
+// Work decomposition: one thread-block CLUSTER of C CTAs (512 threads, one CTA per SM) per
+// (sequence, KV head) unit; C is chosen so the grid fills the 148 SMs in one wave.
 //   phase A  the CTA owning the newest page appends the token's K/V row and updates that
-//            page's min/max metadata (strict compares, first-seen kept);
-//   phase B  each CTA estimates its contiguous range of pages for all G query heads of
-//            the KV head (bitwise fp64 chains, as estimate.cu) and writes the scores to an
-//            L2-resident workspace;  -- cluster barrier (release/acquire) --
-//   phase C  every CTA reads the unit's scores back and runs the exact selection
+//            page's min/max metadata in HBM (strict compares, first-seen kept);
+//   phase B  each CTA estimates a contiguous range of the pages that compete on score
+//            (bitwise fp64 chains, see estimate.cu) for all G query heads of the KV head;
+//            the scores stay in the CTA's shared memory;  -- cluster barrier --
+//   phase C  every CTA pulls the unit's scores over DSMEM and runs the exact selection
 //            (select.cuh) itself, so no second exchange is needed;
 //   phase D  each CTA attends its share of every query head's selected pages (warps
 //            stream pages into an online softmax, as attend.cu) and ships its (m, l, o)
 //            partial to rank 0's shared memory over DSMEM;  -- cluster barrier --
 //            rank 0 merges the partials in rank order and writes the output.
-// With C CTAs per unit the metadata and KV streams of a batch-1 layer are spread over
-// 32*C SMs; the two HBM streams are separated only by the selection's dependency.
-// The launch uses programmatic dependent launch so its prologue overlaps the previous
-// kernel's tail; griddepcontrol.wait precedes every read of data a prior kernel wrote.
+// With force_include_recent the newest page never competes on score (top-(K-1) of pages
+// [0, P-1) plus page P-1 == the reference's replace-the-weakest rule, see topk.cu), so its
+// metadata is not estimated at all; when K >= P nothing is estimated.  qk_debug_keep_scores
+// restores the full estimate_all (every page, scores kept in HBM) for parity tests.
+// The launch uses programmatic dependent launch; griddepcontrol.wait precedes every read
+// of data a prior kernel wrote.
 #include "attend_warp.cuh"
 #include "select.cuh"
 
 namespace qk {
 namespace {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
-constexpr int kGroups = 4;
-constexpr uint32_t kMaxFusedK = 512;  // selected pages per query head kept in smem
+constexpr int kMetaGroups = 8;          // channel groups of the metadata pipeline (mbarriers)
+constexpr int kSelThreads = 128;        // one selection group: a warp per scheduler
+constexpr int kSelGroups = kThreads / kSelThreads;
+constexpr int kSelKpt = 16;             // keys per thread of a selection group
+constexpr uint32_t kMaxFusedK = 512;    // selected pages per query head kept in smem
+constexpr uint32_t kMaxCluster = 16;
+constexpr size_t kKeysBudget = 40 * 1024;  // cluster-exchanged selection keys per CTA
+constexpr size_t kMaxSmem = 227 * 1024 - 8 * 1024;  // opt-in limit minus static smem
 
 __device__ __forceinline__ double h2d(__half h) {
     double d;
@@ -41,7 +50,7 @@ __device__ __forceinline__ double h2d(__half h) {
 // subnormal, +-0): the 15 exponent/mantissa bits land in the double's exponent/mantissa
 // fields unbiased (hence the 2^-1008 scale; fp16 subnormals become double subnormals with
 // the same scale) and the sign moves from bit 25 to bit 31 (t + 63*s clears bit 25 and
-// sets bit 31).  Three integer ops instead of one F2F on the 16-lane/clk XU pipe.
+// sets bit 31).  Three integer ops instead of one F2F on the XU pipe.
 __device__ __forceinline__ double h2d_scaled(unsigned short h) {
     const uint32_t t = uint32_t(h) << 10;
     const uint32_t s = t & 0x02000000u;
@@ -52,7 +61,7 @@ __device__ __forceinline__ void stamp(unsigned long long* probe, int slot) {
     if (probe != nullptr && threadIdx.x == 0) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        probe[blockIdx.x * 16 + slot] = t;
+        probe[blockIdx.x * kProbeSlots + slot] = t;
     }
 }
 
@@ -70,80 +79,133 @@ __device__ __forceinline__ void cluster_sync_acqrel() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n"
                  "barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
-__device__ __forceinline__ void st_cluster_f32(float* local_addr, uint32_t rank, float v) {
-    const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(local_addr));
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t map_rank(const void* local_addr, uint32_t rank) {
     uint32_t ra;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
-    asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(ra), "f"(v) : "memory");
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(local_addr)), "r"(rank));
+    return ra;
+}
+__device__ __forceinline__ void st_cluster_f32(float* local_addr, uint32_t rank, float v) {
+    asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(map_rank(local_addr, rank)), "f"(v)
+                 : "memory");
+}
+__device__ __forceinline__ void st_cluster_u64(uint32_t cluster_addr, unsigned long long v) {
+    asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(cluster_addr), "l"(v) : "memory");
+}
+
+// mbarrier + bulk-copy (TMA 1D) helpers.
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "QK_WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra QK_WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
 }
 
 struct FusedParams {
     __half* k_pool;
     __half* v_pool;
     __half* meta;
+    uint32_t* prange;     // [slices][mrow] page magnitude records
     int32_t* len;
     int32_t* len_ticket;
     int32_t* status;
     const __half* q;
     const __half* k_new;  // nullable
     const __half* v_new;
-    double* ws_scores;    // [B][Hq][Pmax]
+    double* ws_scores;    // [B][Hq][Pmax]: score exchange when keys do not fit smem
     void* out;
     int32_t* pages_out;   // nullable
     int32_t* counts_out;  // nullable
     size_t slice_kv, slice_meta;
+    uint32_t mrow;        // pages per metadata row
     uint32_t layer, B, Hkv, S, head_dim, Pmax, capacity, pstride;
     uint32_t k_budget;    // pages per query head (UINT32_MAX: selection disabled)
-    int force, out_dtype;
+    uint32_t key_cap;     // key slots per head in the cluster-exchanged key array (0: HBM)
+    int force, out_dtype, keep_scores;
     float scale_log2;
-    unsigned long long* probe;  // optional [grid][8] globaltimer stamps (phase timing)
+    unsigned long long* probe;  // optional [grid][kProbeSlots] globaltimer stamps
 };
 
-// Dynamic shared memory: [region A: metadata stage | top-K keys] [dq G*D doubles]
-// [selected pages G*kMaxFusedK ints] [partials G*8*(D+2) floats]
+// Dynamic shared memory:
+//   [region A: metadata stage | after the estimate: selection scratch + padded keys]
+//   [keys: G*key_cap u64, written by every CTA of the cluster]
+//   [dq G*D doubles] [selected pages G*kMaxFusedK ints] [partials G*C*(D+2) floats]
+//   [kMetaGroups mbarriers]
 template <int D, int G>
 struct Layout {
-    static constexpr int NROW = (G == 1) ? 1 : 2;
-    static constexpr int PPC = (G == 1) ? 256 : 128;  // pages per estimate chunk
+    static constexpr int NROW = (G == 1) ? 1 : 2;    // metadata rows staged per channel
+    static constexpr int PPC = (G == 1) ? 512 : 256;  // pages per estimate chunk
     static constexpr size_t stage_bytes = size_t(NROW) * D * PPC * 2;
+    static constexpr size_t scratch_bytes =
+        kSelGroups * sizeof(SelectScratch<kSelThreads>) + sizeof(SelectScratch<kThreads>);
     static size_t region_a(uint32_t pmax) {
         const size_t kpt = (pmax + kThreads - 1) / kThreads;
-        const size_t keys = size_t(kThreads) * (kpt + 1) * 8;
-        return stage_bytes > keys ? stage_bytes : keys;
+        const size_t sel = scratch_bytes + size_t(kThreads) * (kpt + 1) * 8;
+        return stage_bytes > sel ? stage_bytes : sel;
     }
-    static size_t bytes(uint32_t pmax) {
-        return region_a(pmax) + size_t(G) * D * 8 + size_t(G) * kMaxFusedK * 4 +
-               size_t(G) * 8 * (D + 2) * 4;
+    static size_t bytes(uint32_t pmax, uint32_t key_cap, uint32_t cluster) {
+        return region_a(pmax) + size_t(G) * key_cap * 8 + size_t(G) * D * 8 +
+               size_t(G) * kMaxFusedK * 4 + size_t(G) * cluster * (D + 2) * 4 + kMetaGroups * 8;
     }
 };
 
 template <int D, int G>
-__global__ void __launch_bounds__(kThreads, 2) decode_fused_kernel(const FusedParams p,
+__global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedParams p,
                                                                     uint32_t region_a_bytes) {
     using LY = Layout<D, G>;
     constexpr int NROW = LY::NROW, PPC = LY::PPC;
-    constexpr int CH_PER_GROUP = D / kGroups;
+    constexpr int CH_PER_GROUP = D / kMetaGroups;
     constexpr int CPR = D / 8;
     extern __shared__ __align__(16) unsigned char smem[];
-    __half* stage = reinterpret_cast<__half*>(smem);                       // [NROW][D][PPC]
-    unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem);  // aliases stage
-    double* dq = reinterpret_cast<double*>(smem + region_a_bytes);        // [G][D]
+    const uint32_t C = cluster_size(), rank = cluster_rank();
+    __half* stage = reinterpret_cast<__half*>(smem);  // [NROW][D][PPC], region A
+    auto* grp_sc = reinterpret_cast<SelectScratch<kSelThreads>*>(smem);  // region A, later
+    auto* big_sc = reinterpret_cast<SelectScratch<kThreads>*>(grp_sc + kSelGroups);
+    unsigned long long* pkeys = reinterpret_cast<unsigned long long*>(big_sc + 1);  // padded
+    unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem + region_a_bytes);
+    double* dq = reinterpret_cast<double*>(keys + size_t(G) * p.key_cap);  // [G][D]
     int32_t* sel = reinterpret_cast<int32_t*>(dq + G * D);                 // [G][kMaxFusedK]
     float* parts = reinterpret_cast<float*>(sel + G * kMaxFusedK);        // [G][C][D+2]
-    __shared__ SelectScratch<kThreads> sc;
+    unsigned long long* mbar = reinterpret_cast<unsigned long long*>(
+        (reinterpret_cast<uintptr_t>(parts + size_t(G) * C * (D + 2)) + 7) & ~uintptr_t(7));
     __shared__ unsigned char need[D];
     __shared__ float s_o[kWarps][D];
     __shared__ float s_m[kWarps], s_l[kWarps];
 
-    const uint32_t C = cluster_size(), rank = cluster_rank();
     const uint32_t unit = blockIdx.x / C;
     const uint32_t b = unit / p.Hkv, kvh = unit % p.Hkv;
     const uint32_t Hq = p.Hkv * G;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const bool append = p.k_new != nullptr;
 
+    // Peers store into this CTA's shared memory during the estimate: the cluster must have
+    // started everywhere first (arrive now, wait just before the first remote store).
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
     // Everything below reads data earlier kernels wrote.
     stamp(p.probe, 0);
+    if (p.probe && tid == 0) p.probe[blockIdx.x * kProbeSlots + 24] = clock64();
     asm volatile("griddepcontrol.wait;" ::: "memory");
     stamp(p.probe, 1);
 
@@ -169,7 +231,14 @@ __global__ void __launch_bounds__(kThreads, 2) decode_fused_kernel(const FusedPa
     // Query heads of this KV head widened to double (exact), and the rows they need.
     // MHA: odd channels take the integer fp16 -> f64 path (h2d_scaled), whose operand is
     // scaled by 2^-1008, so their query weight is pre-scaled by 2^1008 (exact: |q| <
-    // 2^16 keeps it finite).
+    // 2^16 keeps it finite).  Per head also sum|q| and the smallest ulp code of q (the
+    // split-estimate certificate, phase B).
+    __shared__ double s_qabs[G];
+    __shared__ unsigned int s_qcode[G];
+    if (tid < G) {
+        s_qabs[tid] = 0.0;
+        s_qcode[tid] = 31u;
+    }
 #pragma unroll
     for (int j = 0; j < QPT; ++j) {
         const int i = tid + j * kThreads, c = i % D;
@@ -179,6 +248,20 @@ __global__ void __launch_bounds__(kThreads, 2) decode_fused_kernel(const FusedPa
         }
     }
     __syncthreads();
+#pragma unroll
+    for (int j = 0; j < QPT; ++j) {
+        const int i = tid + j * kThreads;  // warp-uniform head: D is a multiple of 32
+        if (i < G * D) {
+            double a = fabs(double(__half2float(qv[j])));
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);  // exact
+            const unsigned int code = __reduce_min_sync(0xffffffffu, ulp_code(__half_as_ushort(qv[j])));
+            if (lane == 0) {
+                atomicAdd(&s_qabs[i / D], a);
+                atomicMin(&s_qcode[i / D], code);
+            }
+        }
+    }
     for (int c = tid; c < D; c += kThreads) {
         unsigned char m = 0;
 #pragma unroll
@@ -186,96 +269,226 @@ __global__ void __launch_bounds__(kThreads, 2) decode_fused_kernel(const FusedPa
         need[c] = m;
     }
     __syncthreads();
+    stamp(p.probe, 2);
 
-    // This CTA's page range, tile aligned.
-    const uint32_t per = ((P + C - 1) / C + kMetaTile - 1) / kMetaTile * kMetaTile;
-    const uint32_t r_begin = min(P, rank * per), r_end = min(P, r_begin + per);
+    // Selection shape (criticality.cpp:47-59): K >= P -> every page; with force-recent
+    // the candidates are pages [0, P-1) and target K-1, page P-1 is appended.
+    const bool all_pages = p.k_budget >= P;
+    const uint32_t count = all_pages ? P : p.k_budget;
+    const uint32_t n_cand = all_pages ? 0u : (p.force ? P - 1 : P);
+    const uint32_t n_est = p.keep_scores ? P : n_cand;
+    const bool smem_keys = p.key_cap != 0 && key_slots(n_cand) <= p.key_cap;
+    // This CTA's estimate range: contiguous, a multiple of 8 pages (16-byte metadata
+    // pieces), balanced over the cluster.
+    const uint32_t per = ((n_est + C - 1) / C + 7) & ~7u;
+    const uint32_t r_begin = min(n_est, rank * per), r_end = min(n_est, r_begin + per);
 
-    // ---- phase A: append into the newest page (owner CTA only) ----------------------
-    // Done after the first metadata chunk's copies are in flight (see phase B); the staged
-    // copy of the newest page is patched with the new min/max before it is used.
+    // ---- phase A: append into the newest page --------------------------------------------
+    // Owner: the CTA whose estimate range holds the newest page (it patches its staged
+    // copy of that page's metadata), else the last CTA.
     const uint32_t new_page = append ? t_old / p.S : 0xffffffffu;
-    const bool owner = append && new_page >= r_begin && new_page < r_end;
-    __half new_min = __float2half(0.0f), new_max = __float2half(0.0f);
+    const uint32_t owner_rank = (append && new_page < n_est) ? new_page / per : C - 1;
+    const bool owner = append && rank == owner_rank;
+    const bool patch = owner && new_page < n_est;  // staged copy to patch
+    __shared__ __half s_new_min[D], s_new_max[D];
+    __shared__ uint32_t s_rec_scratch[D / 32];
+    bool appended = false;
+    auto do_append = [&]() {
+        if (tid < D) {
+            const uint32_t c = tid, row = t_old % p.S;
+            const size_t in = (size_t(b) * p.Hkv + kvh) * p.head_dim + c;
+            const __half x = c < p.head_dim ? p.k_new[in] : __float2half(0.0f);
+            const __half y = c < p.head_dim ? p.v_new[in] : __float2half(0.0f);
+            const size_t kv = s * p.slice_kv + (size_t(new_page) * p.S + row) * D + c;
+            p.k_pool[kv] = x;
+            p.v_pool[kv] = y;
+            __half* mnp = p.meta + meta_offset(p.slice_meta, p.mrow, s, new_page, D, 0, int(c));
+            __half* mxp = p.meta + meta_offset(p.slice_meta, p.mrow, s, new_page, D, 1, int(c));
+            __half new_min = x, new_max = x;
+            if (row != 0) {
+                new_min = *mnp;
+                new_max = *mxp;
+                const float xf = __half2float(x);
+                if (xf < __half2float(new_min)) new_min = x;
+                if (xf > __half2float(new_max)) new_max = x;
+            }
+            *mnp = new_min;
+            *mxp = new_max;
+            s_new_min[c] = new_min;
+            s_new_max[c] = new_max;
+            const uint32_t rec = page_record<D>(new_min, new_max, s_rec_scratch, 6);
+            if (tid == 0) p.prange[s * p.mrow + new_page] = rec;
+        }
+        appended = true;
+    };
 
-    // ---- phase B: estimate this CTA's pages -------------------------------------------
+    // ---- phase B: estimate this CTA's pages --------------------------------------------
+    // All threads stage the needed metadata rows of a chunk with 16-byte cp.async in
+    // kMetaGroups channel groups, then fold the groups into the fp64 sums as they land.
+    //
+    // Split chains.  The reference sums the 128 exact products q_i*x_i sequentially in
+    // fp64 (criticality.cpp:16-21); one dependent DFMA costs ~34 cycles here, so a
+    // sequential chain is ~2.2 us.  Instead each page keeps NACC accumulators over the
+    // channel residues mod NACC and adds them pairwise at the end.  That is bitwise the
+    // sequential sum whenever no partial sum can round: every product is a multiple of
+    // 2^(uq + ux) (uq, ux = the smallest ulp exponents of the query and of the page's
+    // metadata), so if sum_i |q_i|*|x_i| < 2^(53 + uq + ux) every partial sum -- in any order
+    // -- is an exactly representable multiple of 2^(uq+ux).  The bound uses
+    // sum|q| * max|x| from the page's magnitude record; a page that fails it (or the newest
+    // page, patched in shared memory) is recomputed with the sequential chain.
+    constexpr int NACC = (G == 1) ? 8 : 4;
     const __half* mslice = p.meta + s * p.slice_meta;
+    const uint32_t* rslice = p.prange + s * p.mrow;
+    stamp(p.probe, 21);
+    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+    stamp(p.probe, 22);
+    if constexpr (G == 1) {
+        // MHA: metadata straight into registers.  Lane (pb, cg) of warp w owns pages
+        // base + 8*pb .. +7 (base = c0 + 32w) over channels [cg*CPG, cg*CPG + CPG): one
+        // 16-byte load per channel of its sign-selected row; every warp keeps its loads in
+        // flight at once (no shared-memory staging, no per-group barriers).  The 8 channel
+        // groups of a page are then added with a shuffle transpose (exact under the
+        // certificate; failing pages take the sequential chain).
+        if (owner && !appended) {
+            do_append();
+            __syncthreads();  // s_new_min/max for the newest page's chain
+        }
+        if (r_begin < r_end) stamp(p.probe, 3);
+        constexpr int CPG = D / 8;  // channels per warp
+        const int cg = warp & 7, half = warp >> 3;
+        double* part = reinterpret_cast<double*>(smem);  // [8][512] partial sums (region A)
+        for (uint32_t c0 = r_begin; c0 < r_end; c0 += kThreads) {
+            // Warp (half, cg): pages c0 + 256*half + 8*lane .. +7, channels cg*CPG + [0, CPG):
+            // every load instruction reads 512 contiguous bytes of one metadata row.
+            const uint32_t pbase = c0 + uint32_t(half) * 256 + uint32_t(lane) * 8;
+            const bool act = pbase < r_end;  // pages past r_end are loaded (in-bounds) but unused
+            const uint32_t pg = c0 + uint32_t(tid);  // the page this thread finishes below
+            const uint32_t rec = pg < r_end ? __ldg(rslice + pg) : 0u;  // issued with the rows
+            int4 v[CPG];
+#pragma unroll
+            for (int k = 0; k < CPG; ++k) {
+                const int c = cg * CPG + k;
+                const int minmax = (need[c] & 2) ? 0 : 1;
+                v[k] = act ? ld_nc_v4(mslice + (size_t(minmax) * D + c) * p.mrow + pbase)
+                           : make_int4(0, 0, 0, 0);
+            }
+            double acc[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+#pragma unroll
+            for (int k = 0; k < CPG; ++k) {
+                const int c = cg * CPG + k;
+                const double w = dq[c];
+                const unsigned short* h = reinterpret_cast<const unsigned short*>(&v[k]);
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    acc[j] = __fma_rn(w, (c & 1) ? h2d_scaled(h[j]) : h2d(__ushort_as_half(h[j])), acc[j]);
+            }
+            double2* dst = reinterpret_cast<double2*>(part + cg * kThreads + half * 256 + lane * 8);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dst[j] = make_double2(acc[2 * j], acc[2 * j + 1]);
+            __syncthreads();
+            if (pg < r_end) {
+                double sc = ((part[0 * kThreads + tid] + part[1 * kThreads + tid]) +
+                             (part[2 * kThreads + tid] + part[3 * kThreads + tid])) +
+                            ((part[4 * kThreads + tid] + part[5 * kThreads + tid]) +
+                             (part[6 * kThreads + tid] + part[7 * kThreads + tid]));
+                const uint32_t xcode = rec >> 16, qcode = s_qcode[0];
+                bool exact = xcode >= 31u || qcode >= 31u;
+                if (!exact) {
+                    const double bound = __dmul_ru(
+                        s_qabs[0], double(__half2float(__ushort_as_half(uint16_t(rec & 0x7fffu)))));
+                    const int e = 5 + int(qcode) + int(xcode);
+                    exact = bound < __longlong_as_double(static_cast<long long>(e + 1023) << 52);
+                }
+                const bool newest = patch && pg == new_page;
+                if (!exact || newest) {
+                    if (p.probe) atomicAdd(p.probe + blockIdx.x * kProbeSlots + 23, 1ull);
+                    // The reference's sequential chain (criticality.cpp:16-21).
+                    double a = 0.0;
+                    for (int c = 0; c < D; ++c) {
+                        const int minmax = (need[c] & 2) ? 0 : 1;
+                        const __half x = newest ? (minmax == 0 ? s_new_min[c] : s_new_max[c])
+                                                : mslice[(size_t(minmax) * D + c) * p.mrow + pg];
+                        const double w = (c & 1) ? dq[c] * 0x1p-1008 : dq[c];
+                        a = __fma_rn(w, h2d(x), a);
+                    }
+                    sc = a;
+                }
+                if (smem_keys) {
+                    if (pg < n_cand) {
+                        const unsigned long long k = order_key(sc);
+                        const uint32_t a = smem_u32(keys + key_slot(pg));
+                        for (uint32_t r = 0; r < C; ++r) {
+                            uint32_t ra;
+                            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(r));
+                            st_cluster_u64(ra, k);
+                        }
+                    }
+                }
+                if (!smem_keys || p.keep_scores)
+                    p.ws_scores[(size_t(b) * Hq + size_t(kvh)) * p.Pmax + pg] = sc;
+            }
+            __syncthreads();  // part reused by the next chunk
+        }
+        if (r_begin < r_end) stamp(p.probe, 4);
+    } else {
     for (uint32_t c0 = r_begin; c0 < r_end; c0 += PPC) {
         const uint32_t npg = min(uint32_t(PPC), r_end - c0);
-        const int ntiles = int((npg + kMetaTile - 1) / kMetaTile);
-        constexpr int CHUNKS = kMetaTile * 2 / 16;
+        const int n8 = int((npg + 7) / 8);  // 16-byte pieces per channel row
+        // Thread -> (row, 16-byte piece): piece = tid % PIECES, rows tid / PIECES + k*RSTEP.
+        constexpr int PIECES = PPC / 8, RSTEP = kThreads / PIECES;
+        constexpr int ROWS = CH_PER_GROUP * NROW;  // staged rows per channel group
+        const int my_piece = tid % PIECES;
+        const bool piece_ok = my_piece < n8;
+#pragma unroll 1
+        for (int grp = 0; grp < kMetaGroups; ++grp) {
 #pragma unroll
-        for (int grp = 0; grp < kGroups; ++grp) {
-            const int n_items = ntiles * CH_PER_GROUP * NROW * CHUNKS;
-            for (int i = tid; i < n_items; i += kThreads) {
-                const int part = i % CHUNKS;
-                int rest = i / CHUNKS;
-                const int r = rest % NROW;
-                rest /= NROW;
-                const int c = grp * CH_PER_GROUP + rest % CH_PER_GROUP;
-                const int t = rest / CH_PER_GROUP;
+            for (int rr = tid / PIECES; rr < ROWS; rr += RSTEP) {
+                const int r = rr % NROW;
+                const int c = grp * CH_PER_GROUP + rr / NROW;
                 const int minmax = (G == 1) ? ((need[c] & 2) ? 0 : 1) : r;
-                if (G > 1 && !(need[c] & (minmax == 0 ? 2 : 1))) continue;
-                const __half* src = mslice + (size_t(c0 / kMetaTile + t) * 2 + minmax) * D * kMetaTile +
-                                    size_t(c) * kMetaTile + part * 8;
-                __half* dst = stage + (size_t(r) * D + c) * PPC + t * kMetaTile + part * 8;
-                cp_async16(dst, src);
+                const bool needed = (G == 1) || (need[c] & (minmax == 0 ? 2 : 1));
+                if (piece_ok && needed)
+                    cp_async16(stage + (size_t(r) * D + c) * PPC + my_piece * 8,
+                               mslice + (size_t(minmax) * D + c) * p.mrow + c0 + my_piece * 8);
             }
             cp_async_commit();
         }
-    if (c0 == r_begin && owner && tid < D) {  // phase A, overlapping the copies above
-        const uint32_t c = tid, row = t_old % p.S;
-        const size_t in = (size_t(b) * p.Hkv + kvh) * p.head_dim + c;
-        const __half x = c < p.head_dim ? p.k_new[in] : __float2half(0.0f);
-        const __half y = c < p.head_dim ? p.v_new[in] : __float2half(0.0f);
-        const size_t kv = s * p.slice_kv + (size_t(new_page) * p.S + row) * D + c;
-        p.k_pool[kv] = x;
-        p.v_pool[kv] = y;
-        const size_t mbase = s * p.slice_meta + size_t(new_page / kMetaTile) * 2 * D * kMetaTile +
-                             size_t(c) * kMetaTile + (new_page % kMetaTile);
-        __half* mnp = p.meta + mbase;
-        __half* mxp = p.meta + mbase + size_t(D) * kMetaTile;
-        if (row == 0) {
-            new_min = x;
-            new_max = x;
-        } else {
-            new_min = *mnp;
-            new_max = *mxp;
-            const float xf = __half2float(x);
-            if (xf < __half2float(new_min)) new_min = x;
-            if (xf > __half2float(new_max)) new_max = x;
+        if (c0 == r_begin) stamp(p.probe, 3);
+        if (owner && !appended) {
+            do_append();  // overlaps the copies above
+            __syncthreads();  // s_new_min/max for the patch below
         }
-        *mnp = new_min;
-        *mxp = new_max;
-    }
         // Thread -> (page, query-head subset) of this chunk.
         constexpr int TPP = kThreads / PPC;  // threads per page: 1 (MHA) or 2 (GQA)
         constexpr int GPT = (G + TPP - 1) / TPP;
         const int pi = tid % PPC, gsub = tid / PPC;
+        const uint32_t pg = c0 + pi;
         const bool active = uint32_t(pi) < npg;
-        double acc[GPT];
+        const uint32_t rec = active ? rslice[pg] : 0u;
+        double acc[GPT][NACC];
 #pragma unroll
-        for (int j = 0; j < GPT; ++j) acc[j] = 0.0;
+        for (int j = 0; j < GPT; ++j)
 #pragma unroll
-        for (int grp = 0; grp < kGroups; ++grp) {
-            if (grp == 0) cp_async_wait<kGroups - 1>();
-            if (grp == 1) cp_async_wait<kGroups - 2>();
-            if (grp == 2) cp_async_wait<kGroups - 3>();
-            if (grp == 3) cp_async_wait<0>();
-            __syncthreads();
-            if (owner && new_page >= c0 && new_page < c0 + PPC && tid < D &&
+            for (int k = 0; k < NACC; ++k) acc[j][k] = 0.0;
+#pragma unroll 1
+        for (int grp = 0; grp < kMetaGroups; ++grp) {
+            cp_async_wait_n(kMetaGroups - 1 - grp);
+            if (patch && new_page >= c0 && new_page < c0 + PPC && tid < D &&
                 tid / CH_PER_GROUP == grp) {
                 // Replace the staged (pre-append) metadata of the newest page.
                 const int c = tid;
                 const uint32_t col = new_page - c0;
                 if (G == 1) {
-                    stage[size_t(c) * PPC + col] = (need[c] & 2) ? new_min : new_max;
+                    stage[size_t(c) * PPC + col] = (need[c] & 2) ? s_new_min[c] : s_new_max[c];
                 } else {
-                    stage[size_t(0 * D + c) * PPC + col] = new_min;
-                    stage[size_t(1 * D + c) * PPC + col] = new_max;
+                    stage[size_t(0 * D + c) * PPC + col] = s_new_min[c];
+                    stage[size_t(1 * D + c) * PPC + col] = s_new_max[c];
                 }
             }
-            if (owner) __syncthreads();
+            __syncthreads();
+            if (c0 == r_begin && grp < 4) stamp(p.probe, 4 + grp);
             if (active && G == 1) {
                 // Channel pairs: the even one converts on the XU pipe (F2F), the odd one
                 // with three integer ops (h2d_scaled), so the two pipes share the work.
@@ -286,23 +499,21 @@ __global__ void __launch_bounds__(kThreads, 2) decode_fused_kernel(const FusedPa
                     const double2 w = *reinterpret_cast<const double2*>(dq + c);
                     const unsigned short h0 = st16[size_t(c) * PPC + pi];
                     const unsigned short h1 = st16[size_t(c + 1) * PPC + pi];
-                    acc[0] = __fma_rn(w.x, h2d(__ushort_as_half(h0)), acc[0]);
-                    acc[0] = __fma_rn(w.y, h2d_scaled(h1), acc[0]);
+                    acc[0][cc % NACC] = __fma_rn(w.x, h2d(__ushort_as_half(h0)), acc[0][cc % NACC]);
+                    acc[0][(cc + 1) % NACC] = __fma_rn(w.y, h2d_scaled(h1), acc[0][(cc + 1) % NACC]);
                 }
             } else if (active) {
-#pragma unroll 4
+#pragma unroll
                 for (int cc = 0; cc < CH_PER_GROUP; ++cc) {
                     const int c = grp * CH_PER_GROUP + cc;
-                    {
-                        const double lo = h2d(stage[size_t(c) * PPC + pi]);
-                        const double hi = h2d(stage[size_t(D + c) * PPC + pi]);
+                    const double lo = h2d(stage[size_t(c) * PPC + pi]);
+                    const double hi = h2d(stage[size_t(D + c) * PPC + pi]);
 #pragma unroll
-                        for (int j = 0; j < GPT; ++j) {
-                            const int g = gsub * GPT + j;
-                            if (g < G) {
-                                const double w = dq[g * D + c];
-                                acc[j] = __fma_rn(w, (w < 0.0) ? lo : hi, acc[j]);
-                            }
+                    for (int j = 0; j < GPT; ++j) {
+                        const int g = gsub * GPT + j;
+                        if (g < G) {
+                            const double w = dq[g * D + c];
+                            acc[j][cc % NACC] = __fma_rn(w, (w < 0.0) ? lo : hi, acc[j][cc % NACC]);
                         }
                     }
                 }
@@ -312,18 +523,65 @@ __global__ void __launch_bounds__(kThreads, 2) decode_fused_kernel(const FusedPa
 #pragma unroll
             for (int j = 0; j < GPT; ++j) {
                 const int g = gsub * GPT + j;
-                if (g < G)
-                    p.ws_scores[(size_t(b) * Hq + size_t(kvh) * G + g) * p.Pmax + c0 + pi] = acc[j];
+                if (g < G) {
+                    double sc;
+                    if (NACC == 8)
+                        sc = ((acc[j][0] + acc[j][1]) + (acc[j][2] + acc[j][3])) +
+                             ((acc[j][4 % NACC] + acc[j][5 % NACC]) + (acc[j][6 % NACC] + acc[j][7 % NACC]));
+                    else
+                        sc = (acc[j][0] + acc[j][1]) + (acc[j][2] + acc[j][3]);
+                    // Certificate: sum|q| * max|x| < 2^(53 + uq + ux), ulp = 2^(code - 24).
+                    const uint32_t xcode = rec >> 16, qcode = s_qcode[g];
+                    bool exact = xcode >= 31u || qcode >= 31u;  // all-zero operands
+                    if (!exact) {
+                        const double bound = __dmul_ru(
+                            s_qabs[g], double(__half2float(__ushort_as_half(uint16_t(rec & 0x7fffu)))));
+                        const int e = 5 + int(qcode) + int(xcode);  // 53 + (qcode-24) + (xcode-24)
+                        exact = bound < __longlong_as_double(static_cast<long long>(e + 1023) << 52);
+                    }
+                    if (!exact || (patch && pg == new_page)) {
+                        // The sequential chain of the reference, from the staged rows.
+                        double a = 0.0;
+                        for (int c = 0; c < D; ++c) {
+                            const double w = dq[g * D + c];
+                            if (G == 1) {
+                                const unsigned short h = reinterpret_cast<const unsigned short*>(stage)[size_t(c) * PPC + pi];
+                                a = __fma_rn(w, (c & 1) ? h2d_scaled(h) : h2d(__ushort_as_half(h)), a);
+                            } else {
+                                const double lo = h2d(stage[size_t(c) * PPC + pi]);
+                                const double hi = h2d(stage[size_t(D + c) * PPC + pi]);
+                                a = __fma_rn(w, (w < 0.0) ? lo : hi, a);
+                            }
+                        }
+                        sc = a;
+                    }
+                    if (smem_keys) {
+                        if (pg < n_cand) {
+                            // Push the key to every CTA of the cluster (padded slot).
+                            const unsigned long long k = order_key(sc);
+                            const uint32_t a = smem_u32(keys + size_t(g) * p.key_cap + key_slot(pg));
+                            for (uint32_t r = 0; r < C; ++r) {
+                                uint32_t ra;
+                                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(r));
+                                st_cluster_u64(ra, k);
+                            }
+                        }
+                    }
+                    if (!smem_keys || p.keep_scores)
+                        p.ws_scores[(size_t(b) * Hq + size_t(kvh) * G + g) * p.Pmax + pg] = sc;
+                }
             }
         }
         __syncthreads();  // stage reused by the next chunk
     }
+    }  // G > 1
+    if (owner && !appended) do_append();  // an empty estimate range
 
-    // Scores of every CTA of the unit are visible after this barrier (and so is the new
-    // K/V row written in phase A).
-    stamp(p.probe, 2);
+    // Keys of every CTA of the unit are visible after this barrier (and so is the new K/V
+    // row written in phase A).
+    stamp(p.probe, 8);
     cluster_sync_acqrel();
-    stamp(p.probe, 3);
+    stamp(p.probe, 9);
     if (append && rank == 0 && tid == 0) {
         // Every CTA of this unit has read the old length.  The last unit of the sequence
         // to get here publishes the new length for the next step.
@@ -334,22 +592,59 @@ __global__ void __launch_bounds__(kThreads, 2) decode_fused_kernel(const FusedPa
     }
 
     // ---- phase C: selection (redundantly in every CTA of the cluster) ----------------
-    const bool all_pages = p.k_budget >= P;
-    const uint32_t count = all_pages ? P : p.k_budget;
     if (!all_pages) {
-        const uint32_t n_cand = p.force ? P - 1 : P;
         const uint32_t target = p.force ? p.k_budget - 1 : p.k_budget;
-        for (int g = 0; g < G; ++g) {
-            int32_t* list = sel + g * kMaxFusedK;
-            if (target > 0) {
-                unsigned long long kmax, kmin;
-                const double* src = p.ws_scores + (size_t(b) * Hq + size_t(kvh) * G + g) * p.Pmax;
-                const int kpt = load_keys<kThreads>(src, n_cand, keys, sc, &kmax, &kmin);
-                sel_stamp(p.probe, 8);
-                block_select<kThreads>(keys, kpt, n_cand, target, kmax, kmin, list, sc, p.probe);
+        if (target > 0) {
+            if (smem_keys && n_cand <= uint32_t(kSelThreads * kSelKpt)) {
+                // Groups of 128 threads, one head each (GQA heads in parallel).
+                const int grpi = warp / (kSelThreads / 32), gt = tid % kSelThreads;
+                for (int g = grpi; g < G; g += kSelGroups) {
+                    const unsigned long long* kg = keys + size_t(g) * p.key_cap;
+                    unsigned long long k16[kSelKpt];
+                    const ulonglong2* src = reinterpret_cast<const ulonglong2*>(kg + key_slot(uint32_t(gt) * kSelKpt));
+                    const bool has = uint32_t(gt) * kSelKpt < n_cand;  // rows past the keys stay out
+#pragma unroll
+                    for (int j = 0; j < kSelKpt / 2; ++j) {
+                        const ulonglong2 v = has ? src[j] : make_ulonglong2(0ull, 0ull);
+                        k16[2 * j] = v.x;
+                        k16[2 * j + 1] = v.y;
+                    }
+                    if (g == 0) stamp(p.probe, 10);
+                    block_select_reg<kSelThreads, kSelKpt>(k16, n_cand, target, kg[0],
+                                                           sel + g * kMaxFusedK, grp_sc[grpi], gt,
+                                                           1 + grpi, g == 0 ? p.probe : nullptr);
+                    group_sync<kSelThreads>(1 + grpi);  // scratch reuse for the next head
+                }
+            } else if (smem_keys && n_cand <= uint32_t(kThreads * kSelKpt)) {
+                for (int g = 0; g < G; ++g) {
+                    const unsigned long long* kg = keys + size_t(g) * p.key_cap;
+                    unsigned long long k16[kSelKpt];
+                    const ulonglong2* src = reinterpret_cast<const ulonglong2*>(kg + key_slot(uint32_t(tid) * kSelKpt));
+                    const bool has = uint32_t(tid) * kSelKpt < n_cand;
+#pragma unroll
+                    for (int j = 0; j < kSelKpt / 2; ++j) {
+                        const ulonglong2 v = has ? src[j] : make_ulonglong2(0ull, 0ull);
+                        k16[2 * j] = v.x;
+                        k16[2 * j + 1] = v.y;
+                    }
+                    block_select_reg<kThreads, kSelKpt>(k16, n_cand, target, kg[0],
+                                                        sel + g * kMaxFusedK, *big_sc, tid, 0,
+                                                        g == 0 ? p.probe : nullptr);
+                    __syncthreads();
+                }
+            } else {
+                // Scores through HBM/L2 (large page counts, large GQA groups).
+                for (int g = 0; g < G; ++g) {
+                    unsigned long long kmax, kmin;
+                    const double* src = p.ws_scores + (size_t(b) * Hq + size_t(kvh) * G + g) * p.Pmax;
+                    const int kpt = load_keys<kThreads>(src, n_cand, pkeys, *big_sc, &kmax, &kmin);
+                    block_select<kThreads>(pkeys, kpt, n_cand, target, kmax, kmin,
+                                           sel + g * kMaxFusedK, *big_sc,
+                                           g == 0 ? p.probe : nullptr);
+                }
             }
-            if (tid == 0 && p.force) list[target] = int32_t(P - 1);
         }
+        if (tid < G && p.force) sel[tid * kMaxFusedK + target] = int32_t(P - 1);
         __syncthreads();
     }
     if (rank == 0 && (p.pages_out || p.counts_out)) {
@@ -362,7 +657,7 @@ __global__ void __launch_bounds__(kThreads, 2) decode_fused_kernel(const FusedPa
         }
     }
 
-    stamp(p.probe, 4);
+    stamp(p.probe, 16);
     // ---- phase D: attention over this CTA's share of every head's pages ---------------
     const uint32_t i_begin = uint32_t((uint64_t(count) * rank) / C);
     const uint32_t i_end = uint32_t((uint64_t(count) * (rank + 1)) / C);
@@ -392,6 +687,7 @@ __global__ void __launch_bounds__(kThreads, 2) decode_fused_kernel(const FusedPa
             s_l[warp] = l;
         }
         __syncthreads();
+        if (g == 0) stamp(p.probe, 17);
         float M = -CUDART_INF_F;
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) M = fmaxf(M, s_m[w]);
@@ -401,7 +697,7 @@ __global__ void __launch_bounds__(kThreads, 2) decode_fused_kernel(const FusedPa
             wsc[w] = (s_m[w] == -CUDART_INF_F) ? 0.0f : exp2f(s_m[w] - M);
             L += s_l[w] * wsc[w];
         }
-        float* slot = parts + (size_t(g) * 8 + rank) * (D + 2);
+        float* slot = parts + (size_t(g) * C + rank) * (D + 2);
         for (int d = tid; d < D; d += kThreads) {
             float acc = 0.0f;
 #pragma unroll
@@ -421,48 +717,63 @@ __global__ void __launch_bounds__(kThreads, 2) decode_fused_kernel(const FusedPa
         __syncthreads();  // s_o / s_m reused by the next head
     }
     asm volatile("griddepcontrol.launch_dependents;");
-    stamp(p.probe, 5);
-    if (C > 1) cluster_sync_acqrel();
-    stamp(p.probe, 6);
+    stamp(p.probe, 18);
+    if (C > 1) cluster_sync_acqrel();  // partials landed; no CTA reads a peer's smem after
+    stamp(p.probe, 19);
+    if (p.probe && tid == 0) p.probe[blockIdx.x * kProbeSlots + 25] = clock64();
     if (rank != 0) return;
 
     // Rank 0: merge the C partials of every head in rank order.  One thread per head
     // turns the C maxima into weights w_r = exp2(m_r - M) / L; then every channel is a
     // C-term dot product.
-    float* wts = s_o[0];  // [G][8] (s_o is free now)
+    float* wts = s_o[0];  // [G][kMaxCluster] (s_o is free now)
     if (tid < G) {
-        const float* base = parts + size_t(tid) * 8 * (D + 2);
+        const float* base = parts + size_t(tid) * C * (D + 2);
         float Mg = -CUDART_INF_F;
         for (uint32_t r = 0; r < C; ++r) Mg = fmaxf(Mg, base[r * (D + 2)]);
         float Lg = 0.0f;
         for (uint32_t r = 0; r < C; ++r) {
             const float mr = base[r * (D + 2)];
             const float w = (mr == -CUDART_INF_F) ? 0.0f : exp2f(mr - Mg);
-            wts[tid * 8 + r] = w;
+            wts[tid * kMaxCluster + r] = w;
             Lg += base[r * (D + 2) + 1] * w;
         }
         const float inv = 1.0f / Lg;
-        for (uint32_t r = 0; r < C; ++r) wts[tid * 8 + r] *= inv;
+        for (uint32_t r = 0; r < C; ++r) wts[tid * kMaxCluster + r] *= inv;
     }
     __syncthreads();
     for (int i = tid; i < G * int(p.head_dim); i += kThreads) {
         const int g = i / int(p.head_dim), d = i % int(p.head_dim);
         const size_t bh = size_t(b) * Hq + size_t(kvh) * G + g;
-        const float* base = parts + size_t(g) * 8 * (D + 2) + 2 + d;
+        const float* base = parts + size_t(g) * C * (D + 2) + 2 + d;
         float acc = 0.0f;
-        for (uint32_t r = 0; r < C; ++r) acc = fmaf(base[r * (D + 2)], wts[g * 8 + r], acc);
+        for (uint32_t r = 0; r < C; ++r) acc = fmaf(base[r * (D + 2)], wts[g * kMaxCluster + r], acc);
         if (p.out_dtype == QK_DTYPE_F32) static_cast<float*>(p.out)[bh * p.head_dim + d] = acc;
         else static_cast<__half*>(p.out)[bh * p.head_dim + d] = __float2half_rn(acc);
     }
-    stamp(p.probe, 7);
+    stamp(p.probe, 20);
 }
 
 template <int D, int G>
-int run_fused(qk_cache* c, const FusedParams& prm, uint32_t batch, uint32_t cluster,
-              cudaStream_t st) {
+int run_fused(qk_cache* c, FusedParams prm, uint32_t batch, uint32_t cluster,
+              uint32_t max_pages, cudaStream_t st) {
     using LY = Layout<D, G>;
+    // Selection keys of every head exchanged through the cluster's shared memory when they
+    // fit (max_pages bounds the candidates of this launch; graph replays that outgrow it
+    // take the HBM path inside the kernel).
+    const uint32_t cap = (key_slots(max_pages) + 1) & ~1u;  // even: 16-byte aligned rows
+    prm.key_cap = (size_t(G) * cap * 8 <= kKeysBudget) ? cap : 0u;
     const size_t region_a = LY::region_a(c->Pmax);
-    const size_t smem = LY::bytes(c->Pmax);
+    size_t smem = LY::bytes(c->Pmax, prm.key_cap, cluster);
+    while (smem > kMaxSmem && cluster > 1) {  // large GQA groups: fewer partial slots
+        cluster /= 2;
+        smem = LY::bytes(c->Pmax, prm.key_cap, cluster);
+    }
+    if (smem > kMaxSmem && prm.key_cap) {
+        prm.key_cap = 0;
+        smem = LY::bytes(c->Pmax, 0, cluster);
+    }
+    if (smem > kMaxSmem) return set_error(QK_ERR_UNSUPPORTED, "qk_decode_step: shared memory");
     auto kern = decode_fused_kernel<D, G>;
     static size_t configured = 0;
     if (smem > configured) {
@@ -495,18 +806,18 @@ int run_fused(qk_cache* c, const FusedParams& prm, uint32_t batch, uint32_t clus
 
 template <int D>
 int dispatch_g(qk_cache* c, const FusedParams& prm, uint32_t batch, uint32_t cluster,
-               cudaStream_t st) {
+               uint32_t max_pages, cudaStream_t st) {
     switch (c->G) {
-        case 1: return run_fused<D, 1>(c, prm, batch, cluster, st);
-        case 2: return run_fused<D, 2>(c, prm, batch, cluster, st);
-        case 4: return run_fused<D, 4>(c, prm, batch, cluster, st);
-        case 8: return run_fused<D, 8>(c, prm, batch, cluster, st);
+        case 1: return run_fused<D, 1>(c, prm, batch, cluster, max_pages, st);
+        case 2: return run_fused<D, 2>(c, prm, batch, cluster, max_pages, st);
+        case 4: return run_fused<D, 4>(c, prm, batch, cluster, max_pages, st);
+        case 8: return run_fused<D, 8>(c, prm, batch, cluster, max_pages, st);
         default: return set_error(QK_ERR_UNSUPPORTED, "qk_decode_step: GQA group");
     }
 }
 
-// Unfused reference sequence of the same step (used when the fused kernel's limits --
-// kMaxFusedK selected pages per head -- are exceeded).
+// Unfused sequence of the same step (used when the fused kernel's limits -- kMaxFusedK
+// selected pages per head, head_dim 64/128 -- are exceeded).
 int decode_unfused(qk_cache* c, uint32_t layer, const __half* q, const __half* k,
                    const __half* v, uint32_t batch, const qk_selection_cfg& cfg,
                    uint32_t max_pages, void* out, int out_dtype, int32_t* pages,
@@ -531,14 +842,12 @@ int decode_unfused(qk_cache* c, uint32_t layer, const __half* q, const __half* k
 
 }  // namespace
 
-// Cluster size: enough CTAs per unit to put ~2 CTAs on every SM at batch 1, at most 8,
-// and never more than the pages warrant (one 64-page tile per CTA minimum).
+// Cluster size: the largest power of two (<= 16) that keeps one wave of one CTA per SM
+// (units * C <= 148) and leaves every CTA at least 64 pages to estimate.
 uint32_t fused_cluster_size(const qk_cache* c, uint32_t batch, uint32_t pages) {
     const uint32_t units = batch * c->Hkv;
     uint32_t cl = 1;
-    while (cl < 8 && units * cl * 2 <= 2 * 148 && (pages + cl * 2 * kMetaTile - 1) / (cl * 2 * kMetaTile) >= 1 &&
-           pages > cl * kMetaTile)
-        cl *= 2;
+    while (cl * 2 <= kMaxCluster && units * cl * 2 <= 148 && pages >= cl * 2 * 64) cl *= 2;
     return cl;
 }
 
@@ -555,6 +864,7 @@ int launch_decode(qk_cache* c, uint32_t layer, const __half* q, const __half* k,
     prm.k_pool = c->k_pool;
     prm.v_pool = c->v_pool;
     prm.meta = c->meta;
+    prm.prange = c->prange;
     prm.len = c->d_len;
     prm.len_ticket = c->len_ticket;
     prm.status = c->d_status;
@@ -567,6 +877,7 @@ int launch_decode(qk_cache* c, uint32_t layer, const __half* q, const __half* k,
     prm.counts_out = counts;
     prm.slice_kv = c->slice_kv;
     prm.slice_meta = c->slice_meta;
+    prm.mrow = c->Mrow;
     prm.layer = layer;
     prm.B = c->B;
     prm.Hkv = c->Hkv;
@@ -578,12 +889,13 @@ int launch_decode(qk_cache* c, uint32_t layer, const __half* q, const __half* k,
     prm.k_budget = kk;
     prm.force = cfg.force_include_recent ? 1 : 0;
     prm.out_dtype = out_dtype;
+    prm.keep_scores = c->keep_scores ? 1 : 0;
     prm.scale_log2 = float(1.4426950408889634 / sqrt(double(c->desc.head_dim)));
     prm.probe = c->probe;
     const uint32_t cluster = fused_cluster_size(c, batch, max_pages);
     switch (c->D) {
-        case 64: return dispatch_g<64>(c, prm, batch, cluster, st);
-        case 128: return dispatch_g<128>(c, prm, batch, cluster, st);
+        case 64: return dispatch_g<64>(c, prm, batch, cluster, max_pages, st);
+        case 128: return dispatch_g<128>(c, prm, batch, cluster, max_pages, st);
         default: return set_error(QK_ERR_UNSUPPORTED, "qk_decode_step: head_dim");
     }
 }

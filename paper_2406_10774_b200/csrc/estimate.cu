@@ -15,8 +15,8 @@
 //     metadata bytes the reference's accounting charges (metrics.cpp:105).
 //   * The fp64 chain per (query head, page) runs channel 0..D-1 in order in one thread.
 //
-// Work layout: one CTA per (64*TILES pages, sequence, KV head); 128 threads.  The needed
-// metadata rows (128 contiguous bytes per channel per tile) are staged into shared
+// Work layout: one CTA per (PAGES pages, sequence, KV head); 128 threads.  The needed
+// metadata rows (one contiguous run of PAGES*2 bytes per channel) are staged into shared
 // memory with cp.async in four channel groups so the fp64 chains of group g overlap the
 // loads of groups g+1.. .  MHA (G=1): each thread owns two adjacent pages (half2 reads,
 // two independent chains).  GQA (G>1): each thread owns one page and G chains, the
@@ -42,17 +42,16 @@ __device__ __forceinline__ double h2d_scaled(unsigned short h) {
 constexpr int kThreads = 128;
 constexpr int kGroups = 4;
 
-template <int D, int G, int TILES>
+template <int D, int G, int PAGES>
 __global__ void __launch_bounds__(kThreads)
 estimate_kernel(const __half* __restrict__ meta, const int32_t* __restrict__ len,
                 const __half* __restrict__ q, double* __restrict__ scores, uint32_t layer,
                 uint32_t B, uint32_t Hkv, uint32_t S, uint32_t head_dim, size_t slice_meta,
-                uint32_t sstride) {
+                uint32_t mrow, uint32_t sstride) {
     constexpr int NROW = (G == 1) ? 1 : 2;  // metadata rows staged per channel
-    constexpr int PAGES = TILES * kMetaTile;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    __half* rows = reinterpret_cast<__half*>(smem_raw);                 // [TILES][NROW][D][64]
-    double* dq = reinterpret_cast<double*>(rows + TILES * NROW * D * kMetaTile);  // [G][D]
+    __half* rows = reinterpret_cast<__half*>(smem_raw);                 // [NROW][D][PAGES]
+    double* dq = reinterpret_cast<double*>(rows + NROW * D * PAGES);    // [G][D]
     __shared__ unsigned char need[D];  // bit0: max row needed, bit1: min row needed
 
     const uint32_t bh = blockIdx.y;
@@ -61,8 +60,8 @@ estimate_kernel(const __half* __restrict__ meta, const int32_t* __restrict__ len
     const uint32_t P = (n_tok + S - 1) / S;
     const uint32_t page0 = blockIdx.x * PAGES;
     if (page0 >= P) return;
-    const uint32_t tile0 = page0 / kMetaTile;
-    const int ntiles = min(TILES, int((P - page0 + kMetaTile - 1) / kMetaTile));
+    const uint32_t npg = min(uint32_t(PAGES), P - page0);
+    const int n8 = int((npg + 7) / 8);  // 16-byte pieces per channel row
 
     // Query of the G heads sharing this KV head, widened to double (exact).
     for (int i = threadIdx.x; i < G * D; i += kThreads) {
@@ -84,25 +83,21 @@ estimate_kernel(const __half* __restrict__ meta, const int32_t* __restrict__ len
     __syncthreads();
 
     const size_t s = (size_t(layer) * B + b) * Hkv + kvh;
-    const __half* mbase = meta + s * slice_meta + size_t(tile0) * 2 * D * kMetaTile;
+    const __half* mslice = meta + s * slice_meta;
     constexpr int CH_PER_GROUP = D / kGroups;
-    constexpr int CHUNKS = kMetaTile * 2 / 16;  // 16-byte chunks per 64-page row (8)
 #pragma unroll
     for (int grp = 0; grp < kGroups; ++grp) {
-        const int n_items = ntiles * CH_PER_GROUP * NROW * CHUNKS;
+        const int n_items = CH_PER_GROUP * NROW * n8;
         for (int i = threadIdx.x; i < n_items; i += kThreads) {
-            const int part = i % CHUNKS;
-            int rest = i / CHUNKS;
+            const int piece = i % n8;
+            const int rest = i / n8;
             const int r = rest % NROW;
-            rest /= NROW;
-            const int c = grp * CH_PER_GROUP + rest % CH_PER_GROUP;
-            const int t = rest / CH_PER_GROUP;
+            const int c = grp * CH_PER_GROUP + rest / NROW;
             // G == 1: the single staged row is the one the query's sign selects.
             const int minmax = (G == 1) ? ((need[c] & 2) ? 0 : 1) : r;
             if (G > 1 && !(need[c] & (minmax == 0 ? 2 : 1))) continue;
-            const __half* src = mbase + (size_t(t) * 2 + minmax) * D * kMetaTile +
-                                size_t(c) * kMetaTile + part * 8;
-            __half* dst = rows + ((size_t(t) * NROW + r) * D + c) * kMetaTile + part * 8;
+            const __half* src = mslice + (size_t(minmax) * D + c) * mrow + page0 + piece * 8;
+            __half* dst = rows + (size_t(r) * D + c) * PAGES + piece * 8;
             cp_async16(dst, src);
         }
         cp_async_commit();
@@ -110,8 +105,7 @@ estimate_kernel(const __half* __restrict__ meta, const int32_t* __restrict__ len
 
     if constexpr (G == 1) {
         const int j = threadIdx.x * 2;  // two adjacent pages
-        const int t = j / kMetaTile, pi = j % kMetaTile;
-        const bool active = t < ntiles;
+        const bool active = uint32_t(j) < npg;
         double acc0 = 0.0, acc1 = 0.0;
 #pragma unroll
         for (int grp = 0; grp < kGroups; ++grp) {
@@ -124,8 +118,7 @@ estimate_kernel(const __half* __restrict__ meta, const int32_t* __restrict__ len
 #pragma unroll 8
                 for (int cc = 0; cc < CH_PER_GROUP; ++cc) {
                     const int c = grp * CH_PER_GROUP + cc;
-                    const __half2 h2 = *reinterpret_cast<const __half2*>(
-                        rows + (size_t(t) * D + c) * kMetaTile + pi);
+                    const __half2 h2 = *reinterpret_cast<const __half2*>(rows + size_t(c) * PAGES + j);
                     // Page 2j converts on the XU pipe, page 2j+1 with integer ops
                     // (h2d_scaled, weight pre-scaled by 2^1008): both pipes share the work.
                     acc0 = __fma_rn(dq[c], h2d(__low2half(h2)), acc0);
@@ -138,9 +131,8 @@ estimate_kernel(const __half* __restrict__ meta, const int32_t* __restrict__ len
         if (active && p < P && p < sstride) out[p] = acc0;
         if (active && p + 1 < P && p + 1 < sstride) out[p + 1] = acc1;
     } else {
-        const int j = threadIdx.x;  // TILES*64 == kThreads pages per CTA
-        const int t = j / kMetaTile, pi = j % kMetaTile;
-        const bool active = t < ntiles;
+        const int j = threadIdx.x;  // PAGES == kThreads pages per CTA
+        const bool active = uint32_t(j) < npg;
         double acc[G];
 #pragma unroll
         for (int g = 0; g < G; ++g) acc[g] = 0.0;
@@ -155,8 +147,8 @@ estimate_kernel(const __half* __restrict__ meta, const int32_t* __restrict__ len
 #pragma unroll 4
                 for (int cc = 0; cc < CH_PER_GROUP; ++cc) {
                     const int c = grp * CH_PER_GROUP + cc;
-                    const double lo = h2d(rows[((size_t(t) * 2 + 0) * D + c) * kMetaTile + pi]);
-                    const double hi = h2d(rows[((size_t(t) * 2 + 1) * D + c) * kMetaTile + pi]);
+                    const double lo = h2d(rows[(size_t(0) * D + c) * PAGES + j]);
+                    const double hi = h2d(rows[(size_t(1) * D + c) * PAGES + j]);
 #pragma unroll
                     for (int g = 0; g < G; ++g) {
                         const double w = dq[g * D + c];
@@ -174,22 +166,22 @@ estimate_kernel(const __half* __restrict__ meta, const int32_t* __restrict__ len
     }
 }
 
-template <int D, int G, int TILES>
+template <int D, int G, int PAGES>
 int run(const qk_cache* c, uint32_t layer, const __half* q, uint32_t batch, double* scores,
         uint32_t stride, uint32_t max_pages, cudaStream_t st) {
     constexpr int NROW = (G == 1) ? 1 : 2;
-    const size_t smem = size_t(TILES) * NROW * D * kMetaTile * sizeof(__half) +
+    const size_t smem = size_t(NROW) * D * PAGES * sizeof(__half) +
                         size_t(G == 1 ? 2 : G) * D * sizeof(double);
-    auto kern = estimate_kernel<D, G, TILES>;
+    auto kern = estimate_kernel<D, G, PAGES>;
     static bool configured = false;
     if (!configured) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         configured = true;
     }
-    const uint32_t pages_per_cta = TILES * kMetaTile;
+    const uint32_t pages_per_cta = PAGES;
     const dim3 grid((max_pages + pages_per_cta - 1) / pages_per_cta, batch * c->Hkv);
     kern<<<grid, kThreads, smem, st>>>(c->meta, c->d_len, q, scores, layer, c->B, c->Hkv, c->S,
-                                       c->desc.head_dim, c->slice_meta, stride);
+                                       c->desc.head_dim, c->slice_meta, c->Mrow, stride);
     const_cast<qk_cache*>(c)->launches++;
     return cuda_check(cudaGetLastError(), "estimate_kernel");
 }
@@ -198,10 +190,10 @@ template <int D>
 int dispatch_g(const qk_cache* c, uint32_t layer, const __half* q, uint32_t batch,
                double* scores, uint32_t stride, uint32_t max_pages, cudaStream_t st) {
     switch (c->G) {
-        case 1: return run<D, 1, 4>(c, layer, q, batch, scores, stride, max_pages, st);
-        case 2: return run<D, 2, 2>(c, layer, q, batch, scores, stride, max_pages, st);
-        case 4: return run<D, 4, 2>(c, layer, q, batch, scores, stride, max_pages, st);
-        case 8: return run<D, 8, 2>(c, layer, q, batch, scores, stride, max_pages, st);
+        case 1: return run<D, 1, 2 * kThreads>(c, layer, q, batch, scores, stride, max_pages, st);
+        case 2: return run<D, 2, kThreads>(c, layer, q, batch, scores, stride, max_pages, st);
+        case 4: return run<D, 4, kThreads>(c, layer, q, batch, scores, stride, max_pages, st);
+        case 8: return run<D, 8, kThreads>(c, layer, q, batch, scores, stride, max_pages, st);
         default: return set_error(QK_ERR_UNSUPPORTED, "qk_estimate: GQA group size must be 1, 2, 4 or 8");
     }
 }

@@ -12,21 +12,28 @@
 namespace qk {
 namespace {
 
-__device__ __forceinline__ size_t meta_index(size_t slice_meta, size_t s, uint32_t page,
-                                             int D, int minmax, int c) {
-    return s * slice_meta + size_t(page / kMetaTile) * 2 * D * kMetaTile +
-           size_t(minmax) * D * kMetaTile + size_t(c) * kMetaTile + (page % kMetaTile);
+// Page magnitude record (qk_internal.cuh) of one page, written by thread 0; the block is
+// the page's D channel threads (D = 64, 128 or 256).
+__device__ __forceinline__ void write_record(uint32_t* dst, __half mn, __half mx, int D) {
+    __shared__ uint32_t scratch[8];
+    uint32_t r;
+    if (D == 64) r = page_record<64>(mn, mx, scratch, 1);
+    else if (D == 128) r = page_record<128>(mn, mx, scratch, 1);
+    else r = page_record<256>(mn, mx, scratch, 1);
+    if (threadIdx.x == 0) *dst = r;
 }
+
 
 // One CTA per (sequence, KV head), one thread per channel.  Every CTA of a sequence reads
 // the same token count; the last one to finish (ticket) bumps it, so no CTA can observe
 // the new count early.
 __global__ void append_kernel(__half* __restrict__ kp, __half* __restrict__ vp,
-                              __half* __restrict__ meta, int32_t* __restrict__ len,
+                              __half* __restrict__ meta, uint32_t* __restrict__ prange,
+                              int32_t* __restrict__ len,
                               int32_t* __restrict__ ticket, int32_t* __restrict__ status,
                               const __half* __restrict__ k, const __half* __restrict__ v,
                               uint32_t layer, uint32_t B, uint32_t Hkv, uint32_t S, int D,
-                              uint32_t head_dim, size_t slice_kv, size_t slice_meta,
+                              uint32_t head_dim, size_t slice_kv, size_t slice_meta, uint32_t mrow,
                               uint32_t capacity) {
     __shared__ int last;
     const uint32_t b = blockIdx.x, h = blockIdx.y, c = threadIdx.x;
@@ -43,16 +50,19 @@ __global__ void append_kernel(__half* __restrict__ kp, __half* __restrict__ vp,
     const size_t kv = s * slice_kv + (size_t(page) * S + row) * D + c;
     kp[kv] = x;
     vp[kv] = y;
-    __half* mn = meta + meta_index(slice_meta, s, page, D, 0, c);
-    __half* mx = meta + meta_index(slice_meta, s, page, D, 1, c);
-    if (row == 0) {
-        *mn = x;
-        *mx = x;
-    } else {
+    __half* mn = meta + meta_offset(slice_meta, mrow, s, page, D, 0, c);
+    __half* mx = meta + meta_offset(slice_meta, mrow, s, page, D, 1, c);
+    __half nmn = x, nmx = x;
+    if (row != 0) {
+        nmn = *mn;
+        nmx = *mx;
         const float xf = __half2float(x);
-        if (xf < __half2float(*mn)) *mn = x;
-        if (xf > __half2float(*mx)) *mx = x;
+        if (xf < __half2float(nmn)) nmn = x;
+        if (xf > __half2float(nmx)) nmx = x;
     }
+    *mn = nmn;
+    *mx = nmx;
+    write_record(prange + s * mrow + page, nmn, nmx, D);
     __syncthreads();
     if (c == 0) last = (atomicAdd(ticket + layer * B + b, 1) == int(Hkv) - 1);
     __syncthreads();
@@ -68,11 +78,12 @@ __global__ void append_kernel(__half* __restrict__ kp, __half* __restrict__ vp,
 // when the first page is already partly filled, so the result is bitwise the
 // metadata n single appends would leave.
 __global__ void prefill_kernel(__half* __restrict__ kp, __half* __restrict__ vp,
-                               __half* __restrict__ meta, int32_t* __restrict__ len,
+                               __half* __restrict__ meta, uint32_t* __restrict__ prange,
+                               int32_t* __restrict__ len,
                                const __half* __restrict__ k, const __half* __restrict__ v,
                                uint32_t layer, uint32_t seq, uint32_t B, uint32_t Hkv,
                                uint32_t S, int D, uint32_t head_dim, size_t slice_kv,
-                               size_t slice_meta, uint32_t t0, uint32_t n) {
+                               size_t slice_meta, uint32_t mrow, uint32_t t0, uint32_t n) {
     const uint32_t page = t0 / S + blockIdx.x;
     const uint32_t h = blockIdx.y;
     const uint32_t c = threadIdx.x;
@@ -81,8 +92,8 @@ __global__ void prefill_kernel(__half* __restrict__ kp, __half* __restrict__ vp,
     const uint32_t page_end = page * S + S;
     const uint32_t r_end = (t0 + n < page_end) ? (t0 + n - page * S) : S;
     __half mn = __float2half(0.0f), mx = __float2half(0.0f);
-    __half* mnp = meta + meta_index(slice_meta, s, page, D, 0, c);
-    __half* mxp = meta + meta_index(slice_meta, s, page, D, 1, c);
+    __half* mnp = meta + meta_offset(slice_meta, mrow, s, page, D, 0, c);
+    __half* mxp = meta + meta_offset(slice_meta, mrow, s, page, D, 1, c);
     if (r_begin != 0) {
         mn = *mnp;
         mx = *mxp;
@@ -106,6 +117,7 @@ __global__ void prefill_kernel(__half* __restrict__ kp, __half* __restrict__ vp,
     }
     *mnp = mn;
     *mxp = mx;
+    write_record(prange + s * mrow + page, mn, mx, D);
     if (blockIdx.x == 0 && blockIdx.y == 0 && c == 0) len[layer * B + seq] = int32_t(t0 + n);
 }
 
@@ -114,8 +126,8 @@ __global__ void prefill_kernel(__half* __restrict__ kp, __half* __restrict__ vp,
 int launch_append(qk_cache* c, uint32_t layer, const __half* k, const __half* v,
                   uint32_t batch, cudaStream_t st) {
     append_kernel<<<dim3(batch, c->Hkv), c->D, 0, st>>>(
-        c->k_pool, c->v_pool, c->meta, c->d_len, c->len_ticket, c->d_status, k, v, layer, c->B,
-        c->Hkv, c->S, c->D, c->desc.head_dim, c->slice_kv, c->slice_meta, c->desc.max_tokens);
+        c->k_pool, c->v_pool, c->meta, c->prange, c->d_len, c->len_ticket, c->d_status, k, v, layer, c->B,
+        c->Hkv, c->S, c->D, c->desc.head_dim, c->slice_kv, c->slice_meta, c->Mrow, c->desc.max_tokens);
     c->launches++;
     return cuda_check(cudaGetLastError(), "append_kernel");
 }
@@ -124,8 +136,8 @@ int launch_prefill(qk_cache* c, uint32_t layer, uint32_t seq, const __half* k,
                    const __half* v, uint32_t n, uint32_t t0, cudaStream_t st) {
     const uint32_t pages = (t0 + n - 1) / c->S - t0 / c->S + 1;
     prefill_kernel<<<dim3(pages, c->Hkv), c->D, 0, st>>>(
-        c->k_pool, c->v_pool, c->meta, c->d_len, k, v, layer, seq, c->B, c->Hkv, c->S, c->D,
-        c->desc.head_dim, c->slice_kv, c->slice_meta, t0, n);
+        c->k_pool, c->v_pool, c->meta, c->prange, c->d_len, k, v, layer, seq, c->B, c->Hkv, c->S, c->D,
+        c->desc.head_dim, c->slice_kv, c->slice_meta, c->Mrow, t0, n);
     c->launches++;
     return cuda_check(cudaGetLastError(), "prefill_kernel");
 }

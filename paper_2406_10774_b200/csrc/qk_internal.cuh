@@ -4,11 +4,14 @@
 // num_kv_heads + kv_head, D = head_dim padded up to 64/128/256 with zero channels:
 //   K pool   k_pool[s][Pmax][S][D]           one page = S*D*2 contiguous bytes (4 KiB at
 //   V pool   v_pool[s][Pmax][S][D]           S=16, D=128), the unit of a page fetch
-//   metadata meta[s][Pmax/64][2][D][64]       channel-major tiles of 64 pages: row
-//                                            (tile, minmax, c) holds channel c of 64
-//                                            consecutive pages (128 contiguous bytes), so
-//                                            the estimate kernel reads, per channel, only
-//                                            the row the query's sign selects
+//   metadata meta[s][2][D][Mrow]              channel-major: row (minmax, c) holds channel
+//                                            c of every page of the slice (Mrow = Pmax
+//                                            rounded up to 64), so a CTA estimating a page
+//                                            range reads, per channel, one contiguous run
+//                                            of the row the query's sign selects
+//   prange   prange[s][Mrow] u32              per-page magnitude record of the metadata
+//                                            (page_record below), the certificate that
+//                                            lets the fused estimate split its fp64 chain
 //   lengths  len[layer][seq]                 int32 token counts (device copy; the host
 //                                            keeps a shadow for validation / grid sizing)
 // Zero padding channels never change a result: padded q is 0, so every estimate term
@@ -27,9 +30,11 @@
 
 namespace qk {
 
-constexpr int kMetaTile = 64;       // pages per metadata tile
+constexpr int kMetaAlign = 64;      // metadata rows are padded to a multiple of 64 pages
 constexpr int kMaxSplits = 64;      // split-KV partitions per (sequence, query head)
 constexpr int kMinPagesPerSplit = 8;
+constexpr uint32_t kMaxClusterCtas = 16;  // fused decode: CTAs per (sequence, KV head)
+constexpr int kProbeSlots = 32;           // QK_PROBE globaltimer stamps per fused CTA
 constexpr uint32_t kMaxPages = 16384;  // top-K keeps one slice's scores in shared memory
 
 struct Status {
@@ -47,12 +52,13 @@ struct qk_cache {
     int D = 0;               // padded head dim
     uint32_t S = 0, L = 0, B = 0, Hq = 0, Hkv = 0, G = 0;
     uint32_t Pmax = 0;       // logical pages per slice
-    uint32_t Ptiles = 0;     // metadata tiles per slice
+    uint32_t Mrow = 0;       // pages per metadata row (Pmax rounded up to kMetaAlign)
     size_t slice_kv = 0;     // halves per slice in k_pool / v_pool
     size_t slice_meta = 0;   // halves per slice in meta
     __half* k_pool = nullptr;
     __half* v_pool = nullptr;
     __half* meta = nullptr;
+    uint32_t* prange = nullptr;          // [slices][Mrow] per-page magnitude records
     int32_t* d_len = nullptr;            // [L][B]
     std::vector<uint32_t> h_len;         // host shadow [L][B]
     float* ws_partial = nullptr;         // [B][Hq][kMaxSplits][D + 2]
@@ -64,7 +70,9 @@ struct qk_cache {
     int32_t* ws_counts = nullptr;        // [B][Hq]
     uint16_t* ws_io = nullptr;           // staging for qk_decode_step_host
     float* ws_out = nullptr;             // [B][Hq][head_dim] fp32
+    float* ws_lse = nullptr;             // [B][Hq] fp32 (host-buffer entry points)
     unsigned long long* probe = nullptr; // phase timestamps of the fused kernel (QK_PROBE)
+    bool keep_scores = false;            // fused step: estimate every page, keep scores
     uint64_t device_bytes = 0;
     std::atomic<uint64_t> launches{0};
 
@@ -107,6 +115,47 @@ int launch_decode(qk_cache* c, uint32_t layer, const __half* q, const __half* k,
 
 namespace qk {
 
+// Offset (halves) of channel c of page `page` in the min (minmax 0) or max (1) row of
+// slice s: meta[s][minmax][D][mrow].
+__host__ __device__ __forceinline__ size_t meta_offset(size_t slice_meta, uint32_t mrow, size_t s,
+                                                       uint32_t page, int D, int minmax, int c) {
+    return s * slice_meta + (size_t(minmax) * D + c) * mrow + page;
+}
+
+// Per-page magnitude record: bits 0..14 = the largest |x| (fp16 magnitude bits) over the
+// page's min and max rows, bits 16..20 = the smallest ulp code over their nonzero values
+// (ulp(x) = 2^(code - 24)), 31 when every value is zero.  Computed from the final min/max
+// rows by every writer of metadata (append, prefill, the fused step's append).
+__device__ __forceinline__ uint32_t ulp_code(uint16_t h) {
+    const uint32_t m = h & 0x7fffu;
+    if (m == 0) return 31u;
+    const uint32_t e = m >> 10;
+    return e == 0 ? 0u : e - 1u;
+}
+
+// Reduction of the record over the NT threads [0, NT) holding one channel's (min, max)
+// each; `scratch` holds NT/32 words; barrier `bar` spans those threads.  Returns the record
+// in every participating thread.
+template <int NT>
+__device__ __forceinline__ uint32_t page_record(__half mn, __half mx, uint32_t* scratch, int bar) {
+    const uint16_t a = __half_as_ushort(mn), b = __half_as_ushort(mx);
+    const uint32_t mag = max(uint32_t(a & 0x7fffu), uint32_t(b & 0x7fffu));
+    const uint32_t code = min(ulp_code(a), ulp_code(b));
+    const uint32_t wmag = __reduce_max_sync(0xffffffffu, mag);
+    const uint32_t wcode = __reduce_min_sync(0xffffffffu, code);
+    if ((threadIdx.x & 31) == 0) scratch[threadIdx.x >> 5] = wmag | (wcode << 16);
+    asm volatile("bar.sync %0, %1;" ::"r"(bar), "n"(NT) : "memory");
+    uint32_t m = 0, c = 31u;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) {
+        const uint32_t r = scratch[w];
+        m = max(m, r & 0xffffu);
+        c = min(c, r >> 16);
+    }
+    asm volatile("bar.sync %0, %1;" ::"r"(bar), "n"(NT) : "memory");  // scratch reusable
+    return m | (c << 16);
+}
+
 __device__ __forceinline__ void record_status(int32_t* status, int32_t code) {
     atomicCAS(status, QK_DEV_OK, code);
 }
@@ -133,6 +182,19 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N));
+}
+// cp.async.wait_group with a run-time count (0..7).
+__device__ __forceinline__ void cp_async_wait_n(int n) {
+    switch (n) {
+        case 0: cp_async_wait<0>(); break;
+        case 1: cp_async_wait<1>(); break;
+        case 2: cp_async_wait<2>(); break;
+        case 3: cp_async_wait<3>(); break;
+        case 4: cp_async_wait<4>(); break;
+        case 5: cp_async_wait<5>(); break;
+        case 6: cp_async_wait<6>(); break;
+        default: cp_async_wait<7>(); break;
+    }
 }
 
 }  // namespace qk

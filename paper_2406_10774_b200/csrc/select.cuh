@@ -22,22 +22,25 @@
 
 namespace qk {
 
-// Optional phase stamps (QK_PROBE): slot 8.. of a 16-slot per-CTA record.
+// Optional phase stamps (QK_PROBE): slots 11..15 of the per-CTA record (decode.cu).
 __device__ __forceinline__ void sel_stamp(unsigned long long* probe, int slot) {
     if (probe != nullptr && threadIdx.x == 0) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        probe[blockIdx.x * 16 + slot] = t;
+        probe[blockIdx.x * kProbeSlots + slot] = t;
     }
 }
 
 template <int NT>
 struct SelectScratch {
-    unsigned int hist[2048];
-    unsigned int warp_sum[NT / 32];
-    unsigned long long red_max[NT / 32], red_min[NT / 32];
+    alignas(16) unsigned int hist[2048];
+    alignas(16) unsigned int warp_sum[NT / 32 < 4 ? 4 : NT / 32];
+    alignas(16) unsigned long long red_max[NT / 32 < 4 ? 4 : NT / 32];
+    unsigned long long red_min[NT / 32 < 4 ? 4 : NT / 32];
     unsigned long long cand_key[32];
     unsigned int cand_idx[32];
+    alignas(16) unsigned long long cand2[64];  // (key, index) pairs of the threshold bin
+    unsigned int cand_take[32];
     unsigned int n_cand;
     unsigned int digit, above, count;
     unsigned long long t_key;
@@ -189,7 +192,7 @@ __device__ void block_select(const unsigned long long* keys, int kpt, uint32_t n
         prefix |= static_cast<unsigned long long>(sc.digit) << lo;
         mask |= static_cast<unsigned long long>(dmask) << lo;
         __syncthreads();
-        sel_stamp(probe, 9 + (pass < 2 ? pass : 2));
+        sel_stamp(probe, 11 + (pass < 2 ? pass : 2));
         ++pass;
         if (bin_count == krem) {
             mode = TAKE_BIN;
@@ -238,7 +241,7 @@ __device__ void block_select(const unsigned long long* keys, int kpt, uint32_t n
         }
         __syncthreads();
     }
-    sel_stamp(probe, 12);
+    sel_stamp(probe, 14);
     const unsigned long long t_key = sc.t_key;
     const unsigned int t_idx = sc.t_idx;
 
@@ -293,7 +296,376 @@ __device__ void block_select(const unsigned long long* keys, int kpt, uint32_t n
         }
     }
     __syncthreads();
-    sel_stamp(probe, 13);
+    sel_stamp(probe, 15);
+}
+
+// Inclusive warp scan of v; lane 31's value is the warp total.
+__device__ __forceinline__ unsigned int warp_incl_scan(unsigned int v) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned int x = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += x;
+    }
+    return v;
+}
+
+// Sum of v[w] over w < upto for the NW (multiple of 4) per-warp values in smem, read as
+// 16-byte broadcast vectors.
+template <int NW>
+__device__ __forceinline__ unsigned int sum_below(const unsigned int* v, int upto) {
+    unsigned int s = 0;
+#pragma unroll
+    for (int w4 = 0; w4 < NW / 4; ++w4) {
+        const uint4 q = reinterpret_cast<const uint4*>(v)[w4];
+        s += (4 * w4 + 0 < upto ? q.x : 0u) + (4 * w4 + 1 < upto ? q.y : 0u) +
+             (4 * w4 + 2 < upto ? q.z : 0u) + (4 * w4 + 3 < upto ? q.w : 0u);
+    }
+    return s;
+}
+
+// Barrier over the NT threads of one selection group (named barrier `id`; id 0 with NT ==
+// blockDim.x is __syncthreads).
+template <int NT>
+__device__ __forceinline__ void group_sync(int id) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(NT) : "memory");
+}
+
+// Padded position of key i in a key array read 16 keys per thread: 2 spare u64 after every
+// 16 keys, so the 16-byte reads of 32 lanes spread over all banks.
+__host__ __device__ __forceinline__ uint32_t key_slot(uint32_t i) { return i + 2u * (i >> 4); }
+__host__ __device__ __forceinline__ uint32_t key_slots(uint32_t n) { return key_slot(n + 15u); }
+
+// Exact top-`target` selection by a group of NT threads (NT/32 warps, gt = thread index in
+// the group, barrier `bar`) over n <= NT*KPT keys held in registers: thread gt owns the keys
+// of indices [gt*KPT, gt*KPT+KPT) (entries >= n are ignored); `ref` is any one of the n
+// keys.  Same result as block_select -- the `target` best by (key desc, index asc), written
+// ascending to out[0..target) -- built for latency: a phase costs one barrier plus the
+// phase's instructions on every warp of the group, so the group is small (128 threads, one
+// warp per scheduler; several groups can select different heads at once) and every step is
+// shuffle-light:
+//   * common key prefix: OR of key ^ ref (redux.sync per warp);
+//   * 11-bit digit histogram (shared atomics); lane l of warp w sums bins of rank
+//     [BPL*(32w + l), +BPL) from the top; the lane holding the krem-th key finds the bin;
+//   * a threshold bin of <= 32 keys is gathered and each of its keys ranks itself;
+//   * ascending compaction from per-thread counts (warp scan + per-warp totals).
+// 1 <= target < n.  out is complete after the group's next barrier.
+template <int NT, int KPT, typename OutT>
+__device__ void block_select_reg_wide(const unsigned long long (&key)[KPT], uint32_t n,
+                                      uint32_t target, unsigned long long ref, OutT* out,
+                                      SelectScratch<NT>& sc, int gt, int bar,
+                                      unsigned long long* probe = nullptr,
+                                      long long* trace = nullptr) {
+#define QK_TRACE(k) \
+    if (trace != nullptr && gt == 0) trace[k] = clock64();
+    constexpr int NW = NT / 32;
+    constexpr int BPL = 2048 / NT;  // histogram bins per lane in the bin search
+    static_assert(NW % 4 == 0 && NW <= 32 && BPL % 4 == 0, "geometry");
+    enum { TAKE_BIN = 0, PAIR = 1, EQUAL = 2 };
+    const int lane = gt & 31, warp = gt >> 5;
+    const uint32_t i0 = uint32_t(gt) * KPT;
+    uint4* hist4 = reinterpret_cast<uint4*>(sc.hist);
+
+    // Zero the histogram; per-warp OR of key ^ ref = the bits where keys differ.
+#pragma unroll
+    for (int j = 0; j < BPL / 4; ++j) hist4[gt * (BPL / 4) + j] = make_uint4(0, 0, 0, 0);
+    if (gt == 0) sc.n_cand = 0;
+    unsigned long long dx = 0;
+#pragma unroll
+    for (int j = 0; j < KPT; ++j)
+        if (i0 + j < n) dx |= key[j] ^ ref;
+    {
+        const unsigned int dhi = __reduce_or_sync(0xffffffffu, unsigned(dx >> 32));
+        const unsigned int dlo = __reduce_or_sync(0xffffffffu, unsigned(dx));
+        if (lane == 0) sc.red_max[warp] = (static_cast<unsigned long long>(dhi) << 32) | dlo;
+    }
+    group_sync<NT>(bar);
+    unsigned long long diff = 0;
+#pragma unroll
+    for (int w2 = 0; w2 < NW / 2; ++w2) {
+        const ulonglong2 q = reinterpret_cast<const ulonglong2*>(sc.red_max)[w2];
+        diff |= q.x | q.y;
+    }
+    int hb = diff ? 63 - __clzll(static_cast<long long>(diff)) : -1;
+    QK_TRACE(0);
+    unsigned long long mask = (hb >= 63) ? 0ull : (~0ull << (hb + 1));
+    unsigned long long prefix = ref & mask;
+    uint32_t krem = target;
+    int mode = (hb < 0 && n <= 32) ? PAIR : EQUAL;
+    bool resolved = false;
+    int pass = 0;
+    while (hb >= 0) {
+        const int lo = hb >= 10 ? hb - 10 : 0;
+        const unsigned int dmask = (1u << (hb - lo + 1)) - 1u;
+#pragma unroll
+        for (int j = 0; j < KPT; ++j)
+            if (i0 + j < n && (key[j] & mask) == prefix)
+                atomicAdd(&sc.hist[(key[j] >> lo) & dmask], 1u);
+        group_sync<NT>(bar);
+        // This lane's bins, highest first: 2047 - BPL*gt - [0, BPL).
+        unsigned int c[BPL], sl = 0;
+#pragma unroll
+        for (int j4 = 0; j4 < BPL / 4; ++j4) {
+            const uint4 q = hist4[(2047 - BPL * gt) / 4 - j4];
+            c[4 * j4 + 0] = q.w;
+            c[4 * j4 + 1] = q.z;
+            c[4 * j4 + 2] = q.y;
+            c[4 * j4 + 3] = q.x;
+        }
+#pragma unroll
+        for (int j = 0; j < BPL; ++j) sl += c[j];
+        QK_TRACE(1);
+        const unsigned int incl = warp_incl_scan(sl);
+        if (lane == 31) sc.warp_sum[warp] = incl;
+        QK_TRACE(2);
+        group_sync<NT>(bar);
+        unsigned int above = sum_below<NW>(sc.warp_sum, warp) + incl - sl;
+        QK_TRACE(3);
+        if (above < krem && krem <= above + sl) {  // exactly one lane of the group
+#pragma unroll
+            for (int j = 0; j < BPL; ++j) {
+                if (above < krem && krem <= above + c[j]) {
+                    sc.count = c[j];
+                    sc.digit = 2047 - (BPL * gt + j);
+                    sc.above = above;
+                }
+                above += c[j];
+            }
+        }
+        group_sync<NT>(bar);
+        krem -= sc.above;
+        const uint32_t bin_count = sc.count;
+        prefix |= static_cast<unsigned long long>(sc.digit) << lo;
+        mask |= static_cast<unsigned long long>(dmask) << lo;
+        QK_TRACE(4);
+        sel_stamp(probe, 11 + (pass < 2 ? pass : 2));
+        ++pass;
+        if (bin_count == krem) {
+            mode = TAKE_BIN;
+            resolved = true;
+            break;
+        }
+        if (bin_count <= 32) {
+            mode = PAIR;
+            break;
+        }
+        hb = lo - 1;
+        if (hb < 0) {
+            mode = EQUAL;  // > 32 keys share one 64-bit value
+            break;
+        }
+        // Next pass: re-zero the histogram once everyone has read it and sc.*.
+        group_sync<NT>(bar);
+#pragma unroll
+        for (int j = 0; j < BPL / 4; ++j) hist4[gt * (BPL / 4) + j] = make_uint4(0, 0, 0, 0);
+        group_sync<NT>(bar);
+    }
+
+    // Per key: selected?  Keys above the threshold bin always; keys of the bin by mode.
+    bool take[KPT];
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) take[j] = (i0 + j < n) && (key[j] & mask) > prefix;
+    if (resolved) {
+#pragma unroll
+        for (int j = 0; j < KPT; ++j) take[j] = take[j] || ((i0 + j < n) && (key[j] & mask) == prefix);
+    } else if (mode == PAIR) {
+        // Gather the <= 32 keys of the bin (sc.n_cand was zeroed before the first barrier
+        // and is untouched since); thread m ranks candidate m; owners read the verdicts.
+        int slot[KPT];
+#pragma unroll
+        for (int j = 0; j < KPT; ++j) {
+            slot[j] = -1;
+            if (i0 + j < n && (key[j] & mask) == prefix) {
+                slot[j] = int(atomicAdd(&sc.n_cand, 1u));
+                reinterpret_cast<ulonglong2*>(sc.cand2)[slot[j]] = make_ulonglong2(key[j], i0 + j);
+            }
+        }
+        group_sync<NT>(bar);
+        const unsigned int nc = sc.n_cand;
+        QK_TRACE(5);
+        if (uint32_t(gt) < nc) {
+            const ulonglong2 me = reinterpret_cast<const ulonglong2*>(sc.cand2)[gt];
+            unsigned int rank = 0;
+#pragma unroll
+            for (int m = 0; m < 32; ++m) {
+                if (uint32_t(m) < nc) {
+                    const ulonglong2 o = reinterpret_cast<const ulonglong2*>(sc.cand2)[m];
+                    rank += (o.x > me.x) || (o.x == me.x && o.y < me.y);
+                }
+            }
+            sc.cand_take[gt] = rank < krem;
+        }
+        group_sync<NT>(bar);
+#pragma unroll
+        for (int j = 0; j < KPT; ++j)
+            if (slot[j] >= 0) take[j] = sc.cand_take[slot[j]] != 0;
+    } else {
+        // EQUAL: the krem lowest indices of the bin.
+        unsigned int e = 0;
+#pragma unroll
+        for (int j = 0; j < KPT; ++j) e += (i0 + j < n) && (key[j] & mask) == prefix;
+        const unsigned int incl = warp_incl_scan(e);
+        if (lane == 31) sc.warp_sum[warp] = incl;
+        group_sync<NT>(bar);
+        unsigned int eq = sum_below<NW>(sc.warp_sum, warp) + incl - e;
+#pragma unroll
+        for (int j = 0; j < KPT; ++j)
+            if (i0 + j < n && (key[j] & mask) == prefix) take[j] = eq++ < krem;
+        group_sync<NT>(bar);  // warp_sum is rewritten below
+    }
+    QK_TRACE(6);
+    sel_stamp(probe, 14);
+
+    // Ascending compaction.
+    unsigned int mine = 0;
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) mine += take[j];
+    const unsigned int incl = warp_incl_scan(mine);
+    if (lane == 31) sc.warp_sum[warp] = incl;
+    QK_TRACE(7);
+    group_sync<NT>(bar);
+    unsigned int pos = sum_below<NW>(sc.warp_sum, warp) + incl - mine;
+    QK_TRACE(8);
+#pragma unroll
+    for (int j = 0; j < KPT; ++j)
+        if (take[j]) out[pos++] = static_cast<OutT>(i0 + j);
+    sel_stamp(probe, 15);
+#undef QK_TRACE
+}
+
+// block_select_reg: the same selection with a 32-bit fast path.  Keys are shifted left
+// past their common prefix once; the first 11-bit radix pass, the bin search and the
+// verdicts then work on the high 32-bit word (one instruction per comparison instead of a
+// 64-bit mask-and-compare).  A pass that leaves more than 32 keys of the threshold bin
+// undecided (heavy ties) restarts in block_select_reg_wide.  Same contract.
+template <int NT, int KPT, typename OutT>
+__device__ void block_select_reg(const unsigned long long (&key)[KPT], uint32_t n, uint32_t target,
+                                 unsigned long long ref, OutT* out, SelectScratch<NT>& sc, int gt,
+                                 int bar, unsigned long long* probe = nullptr) {
+    constexpr int NW = NT / 32;
+    constexpr int BPL = 2048 / NT;
+    static_assert(NW % 4 == 0 && NW <= 32 && BPL % 4 == 0, "geometry");
+    const int lane = gt & 31, warp = gt >> 5;
+    const uint32_t i0 = uint32_t(gt) * KPT;
+    const int nv = n > i0 ? int(min(uint32_t(KPT), n - i0)) : 0;  // valid keys of this thread
+    uint4* hist4 = reinterpret_cast<uint4*>(sc.hist);
+
+#pragma unroll
+    for (int j = 0; j < BPL / 4; ++j) hist4[gt * (BPL / 4) + j] = make_uint4(0, 0, 0, 0);
+    if (gt == 0) sc.n_cand = 0;
+    unsigned long long dx = 0;
+#pragma unroll
+    for (int j = 0; j < KPT; ++j)
+        if (j < nv) dx |= key[j] ^ ref;
+    {
+        const unsigned int dhi = __reduce_or_sync(0xffffffffu, unsigned(dx >> 32));
+        const unsigned int dlo = __reduce_or_sync(0xffffffffu, unsigned(dx));
+        if (lane == 0) sc.red_max[warp] = (static_cast<unsigned long long>(dhi) << 32) | dlo;
+    }
+    group_sync<NT>(bar);
+    unsigned long long diff = 0;
+#pragma unroll
+    for (int w2 = 0; w2 < NW / 2; ++w2) {
+        const ulonglong2 q = reinterpret_cast<const ulonglong2*>(sc.red_max)[w2];
+        diff |= q.x | q.y;
+    }
+    if (diff == 0) {  // every key equal: the lowest indices
+        group_sync<NT>(bar);  // red_max read by all before the wide path reuses sc
+        block_select_reg_wide<NT, KPT>(key, n, target, ref, out, sc, gt, bar, probe);
+        return;
+    }
+    const int shift = __clzll(static_cast<long long>(diff));  // common prefix length
+    unsigned int h[KPT];  // top 32 bits after the common prefix; first digit = h >> 21
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) {
+        h[j] = unsigned((key[j] << shift) >> 32);
+        if (j < nv) atomicAdd(&sc.hist[h[j] >> 21], 1u);
+    }
+    group_sync<NT>(bar);
+    unsigned int c[BPL], sl = 0;
+#pragma unroll
+    for (int j4 = 0; j4 < BPL / 4; ++j4) {
+        const uint4 q = hist4[(2047 - BPL * gt) / 4 - j4];
+        c[4 * j4 + 0] = q.w;
+        c[4 * j4 + 1] = q.z;
+        c[4 * j4 + 2] = q.y;
+        c[4 * j4 + 3] = q.x;
+    }
+#pragma unroll
+    for (int j = 0; j < BPL; ++j) sl += c[j];
+    const unsigned int incl = warp_incl_scan(sl);
+    if (lane == 31) sc.warp_sum[warp] = incl;
+    group_sync<NT>(bar);
+    {
+        unsigned int above = sum_below<NW>(sc.warp_sum, warp) + incl - sl;
+        if (above < target && target <= above + sl) {  // exactly one lane of the group
+#pragma unroll
+            for (int j = 0; j < BPL; ++j) {
+                if (above < target && target <= above + c[j]) {
+                    sc.count = c[j];
+                    sc.digit = 2047 - (BPL * gt + j);
+                    sc.above = above;
+                }
+                above += c[j];
+            }
+        }
+    }
+    group_sync<NT>(bar);
+    const unsigned int bin = sc.digit, bin_count = sc.count;
+    const unsigned int krem = target - sc.above;
+    sel_stamp(probe, 11);
+    if (bin_count != krem && bin_count > 32) {  // needs more digits: the 64-bit path
+        group_sync<NT>(bar);
+        block_select_reg_wide<NT, KPT>(key, n, target, ref, out, sc, gt, bar, probe);
+        return;
+    }
+    // Keys above the bin are in; keys of the bin by TAKE_BIN or by rank (<= 32 keys).
+    bool take[KPT];
+    if (bin_count == krem) {
+#pragma unroll
+        for (int j = 0; j < KPT; ++j) take[j] = j < nv && (h[j] >> 21) >= bin;
+    } else {
+        int slot[KPT];
+#pragma unroll
+        for (int j = 0; j < KPT; ++j) {
+            take[j] = j < nv && (h[j] >> 21) > bin;
+            slot[j] = -1;
+            if (j < nv && (h[j] >> 21) == bin) {
+                slot[j] = int(atomicAdd(&sc.n_cand, 1u));
+                reinterpret_cast<ulonglong2*>(sc.cand2)[slot[j]] = make_ulonglong2(key[j], i0 + j);
+            }
+        }
+        group_sync<NT>(bar);
+        const unsigned int nc = sc.n_cand;
+        if (uint32_t(gt) < nc) {
+            const ulonglong2 me = reinterpret_cast<const ulonglong2*>(sc.cand2)[gt];
+            unsigned int rank = 0;
+#pragma unroll
+            for (int m = 0; m < 32; ++m) {
+                if (uint32_t(m) < nc) {
+                    const ulonglong2 o = reinterpret_cast<const ulonglong2*>(sc.cand2)[m];
+                    rank += (o.x > me.x) || (o.x == me.x && o.y < me.y);
+                }
+            }
+            sc.cand_take[gt] = rank < krem;
+        }
+        group_sync<NT>(bar);
+#pragma unroll
+        for (int j = 0; j < KPT; ++j)
+            if (slot[j] >= 0) take[j] = sc.cand_take[slot[j]] != 0;
+    }
+    sel_stamp(probe, 14);
+    unsigned int mine = 0;
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) mine += take[j];
+    const unsigned int incl2 = warp_incl_scan(mine);
+    if (lane == 31) sc.warp_sum[warp] = incl2;
+    group_sync<NT>(bar);
+    unsigned int pos = sum_below<NW>(sc.warp_sum, warp) + incl2 - mine;
+#pragma unroll
+    for (int j = 0; j < KPT; ++j)
+        if (take[j]) out[pos++] = static_cast<OutT>(i0 + j);
+    sel_stamp(probe, 15);
 }
 
 }  // namespace qk

@@ -274,8 +274,14 @@ class QuestCache:
             _stream_ptr(stream)))
         return out
 
+    def keep_step_scores(self, on: bool = True) -> None:
+        """Make decode_step estimate every page and keep the scores (parity diagnostics;
+        by default the fused step skips scores the selection cannot use)."""
+        check(self._lib.qk_debug_keep_scores(self._h, int(bool(on))))
+
     def step_scores(self, seq: int, q_head: int, n_pages: int, stream=None) -> np.ndarray:
-        """Page scores the last decode_step computed for (seq, q_head) (diagnostics)."""
+        """Page scores the last decode_step computed for (seq, q_head) (diagnostics; needs
+        keep_step_scores())."""
         out = np.empty(n_pages, dtype=np.float64)
         check(self._lib.qk_debug_step_scores(self._h, seq, q_head, out.ctypes.data, n_pages,
                                              _stream_ptr(stream)))

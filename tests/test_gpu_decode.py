@@ -29,9 +29,13 @@ def rel_l2(got, want):
 class Layer:
     """A QuestCache layer plus a host mirror of every slice for the oracle."""
 
-    def __init__(self, qk, rng, B, Hq, Hkv, d, S, lens, extra=16):
+    def __init__(self, qk, rng, B, Hq, Hkv, d, S, lens, extra=16, keep_scores=True):
         self.qc = qk.QuestCache(d, S, max_batch=B, num_q_heads=Hq, num_kv_heads=Hkv,
                                 max_tokens=max(lens) + extra)
+        # keep_scores: estimate every page and keep the scores for a bitwise check; off,
+        # the production path skips the forced page's estimate (pages/outputs checked).
+        self.keep_scores = keep_scores
+        self.qc.keep_step_scores(keep_scores)
         self.B, self.Hq, self.Hkv, self.d, self.S = B, Hq, Hkv, d, S
         self.keys, self.vals = [], []
         sd = 1 / np.sqrt(d)
@@ -70,8 +74,9 @@ class Layer:
                 k, v = self.keys[b][h // G], self.vals[b][h // G]
                 s_want, p_want, o_want = oracle_c.quest_step(q[b, h], k, v, self.S, budget,
                                                              force, enabled)
-                s_got = self.qc.step_scores(b, h, len(s_want))
-                assert np.array_equal(s_got.view(np.uint64), s_want.view(np.uint64)), (b, h)
+                if self.keep_scores:
+                    s_got = self.qc.step_scores(b, h, len(s_want))
+                    assert np.array_equal(s_got.view(np.uint64), s_want.view(np.uint64)), (b, h)
                 got = pages[b, h, : counts[b, h]].tolist()
                 assert got == p_want.tolist(), (b, h)
                 assert rel_l2(out[b, h], o_want) <= TOL, (b, h)
@@ -86,13 +91,15 @@ class Layer:
     (1, 2, 2, 128, [40000], 4096),        # long context, cluster of 8, K = 256
     (1, 4, 4, 100, [700], 64),            # padded head_dim
 ])
-def test_fused_step_vs_oracle(qk, oracle_c, B, Hq, Hkv, d, lens, budget):
+@pytest.mark.parametrize("keep", [True, False])
+def test_fused_step_vs_oracle(qk, oracle_c, B, Hq, Hkv, d, lens, budget, keep):
     rng = np.random.default_rng(sum(lens) + 7 * Hq + d)
-    layer = Layer(qk, rng, B, Hq, Hkv, d, 16, lens)
+    layer = Layer(qk, rng, B, Hq, Hkv, d, 16, lens, keep_scores=keep)
     q, out, pages, counts = layer.step(rng, budget)
     layer.check(oracle_c, q, out, pages, counts, budget)
 
 
+@pytest.mark.parametrize("keep", [True, False])
 @pytest.mark.parametrize("budget,force,enabled", [
     (16, True, True),      # K = 1: only the newest page
     (16, False, True),     # K = 1 by score
@@ -100,9 +107,9 @@ def test_fused_step_vs_oracle(qk, oracle_c, B, Hq, Hkv, d, lens, budget):
     (512, True, False),    # selection disabled: dense over every page
     (1 << 20, True, True),  # budget covers the cache
 ])
-def test_fused_selection_modes(qk, oracle_c, budget, force, enabled):
+def test_fused_selection_modes(qk, oracle_c, budget, force, enabled, keep):
     rng = np.random.default_rng(budget + force)
-    layer = Layer(qk, rng, 2, 4, 4, 128, 16, [2500, 97])
+    layer = Layer(qk, rng, 2, 4, 4, 128, 16, [2500, 97], keep_scores=keep)
     q, out, pages, counts = layer.step(rng, budget, force, enabled)
     layer.check(oracle_c, q, out, pages, counts, budget, force, enabled)
 
@@ -136,6 +143,7 @@ def test_fused_scores_adversarial_values(qk, oracle_c, G):
                         np.float32)
     Hkv, d, S, L = 2, 128, 16, 1000
     qc = qk.QuestCache(d, S, num_q_heads=Hkv * G, num_kv_heads=Hkv, max_tokens=L + 1)
+    qc.keep_step_scores(True)
     keys = half(rng.standard_normal((Hkv, L, d)))
     mask = rng.random(keys.shape) < 0.3
     keys[mask] = rng.choice(specials, size=mask.sum())

@@ -40,40 +40,43 @@ q = (torch.randn((args.batch, H, D), generator=g, device=dev) / D ** 0.5).half()
 kn = (torch.randn((args.batch, Hkv, D), generator=g, device=dev) / D ** 0.5).half()
 out = torch.empty((args.batch, H, D), dtype=torch.float32, device=dev)
 torch.cuda.synchronize()
-n = args.batch * Hkv * 8 * 16
+SLOTS = 32
+n = args.batch * Hkv * 16 * SLOTS
 buf = np.zeros(n, dtype=np.uint64)
 lib = _lib.load()
-names = ["wait", "qload+estimate", "barrier1", "select", "attend", "barrier2", "merge"]
+names = {0: "entry", 1: "dep_wait", 2: "prologue", 21: "pre_cwait", 22: "cluster_wait", 3: "cp_issued", 4: "grp0", 5: "grp1",
+         6: "grp2", 7: "grp3", 8: "estimate_end", 9: "barrier1", 10: "keys_pulled",
+         11: "sel_pass0", 12: "sel_pass1", 13: "sel_pass2", 14: "sel_pair", 15: "sel_compact",
+         16: "select_end", 17: "attend_end", 18: "partials", 19: "barrier2", 20: "merged"}
+for _ in range(50):  # clocks up
+    for layer in range(args.layers):
+        qc.decode_step(layer, q, None, None, args.budget, out=out)
+torch.cuda.synchronize()
+lib.qk_debug_probe(qc._h, buf.ctypes.data, n, None)
 res = []
 for rep in range(args.reps):
     for layer in range(args.layers):
         qc.decode_step(layer, q, kn, kn, args.budget, out=out)
         torch.cuda.synchronize()
         lib.qk_debug_probe(qc._h, buf.ctypes.data, n, None)
-        t16 = buf.reshape(-1, 16).astype(np.int64)
-        valid = t16[:, 0] > 0
-        t16 = t16[valid]
-        t = t16[:, :8]
-        # select internals: 3 -> 8 (load keys), 8 -> 9 (pass 1), 9 -> 12 (rest + pair),
-        # 12 -> 13 (compaction), 13 -> 4 (tail)
-        sel = {}
-        for nm, a, b in (("sel.load", 3, 8), ("sel.pass1", 8, 9), ("sel.to_pair", 9, 12),
-                         ("sel.compact", 12, 13), ("sel.tail", 13, 4)):
-            ok = (t16[:, a] > 0) & (t16[:, b] > 0)
-            if ok.any():
-                d = (t16[ok, b] - t16[ok, a]) / 1000.0
-                sel[nm] = round(float(np.median(d)), 2)
+        t = buf.reshape(-1, SLOTS).astype(np.int64)
+        t = t[t[:, 0] > 0]
         t0 = t[:, 0].min()
-        rel = (t - t0) / 1000.0  # us
-        phases = np.diff(t, axis=1) / 1000.0
-        ranks0 = t[:, 7] > 0
-        row = {"total_us": float((t[ranks0, 7].max() - t0) / 1000.0),
-               "start_spread_us": float(rel[:, 0].max())}
-        for i, nm in enumerate(names):
-            col = phases[:, i] if i < 6 else phases[ranks0, i]
-            col = col[col >= 0]
-            row[nm] = (round(float(np.median(col)), 2), round(float(col.max()), 2))
-        row.update(sel)
+        fb = int(t[:, 23].sum())
+        t[:, 23] = 0
+        cyc = (t[:, 25] - t[:, 24]).astype(np.float64)
+        ns = (t[:, 19] - t[:, 0]).astype(np.float64)
+        mhz = float(np.median(cyc / ns * 1000.0))
+        t[:, 24] = 0
+        t[:, 25] = 0
+        row = {"ctas": int(len(t)), "fallback_pages": fb, "sm_mhz": round(mhz),
+               "total_us": round(float((t.max() - t0) / 1000.0), 3)}
+        for k, nm in names.items():
+            col = t[:, k]
+            ok = col > 0
+            if ok.any():
+                rel = (col[ok] - t0) / 1000.0
+                row[nm] = (round(float(np.median(rel)), 2), round(float(rel.max()), 2))
         res.append(row)
 for r in res[-args.layers:]:
     print(json.dumps(r))
