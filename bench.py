@@ -82,28 +82,46 @@ def algorithmic_bytes(lengths, heads, head_dim, page, budget, bpe=2):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled DURING the timed region: NVML in-process every
+    ~2 ms (the timed region lasts tens of ms), nvidia-smi as a fallback."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
 
     def __init__(self, index: int):
         self.index = index
-        self.samples = []
+        self.samples = []  # (sm_mhz, max_mhz, reasons bitmask)
         self._stop = threading.Event()
         self._t = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        except Exception:
+            self._nvml = None
+
+    def _sample(self):
+        if self._nvml is not None:
+            n = self._nvml
+            sm = n.nvmlDeviceGetClockInfo(self._h, n.NVML_CLOCK_SM)
+            mx = n.nvmlDeviceGetMaxClockInfo(self._h, n.NVML_CLOCK_SM)
+            rs = n.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            return float(sm), float(mx), int(rs)
+        out = subprocess.run(
+            ["nvidia-smi", f"--id={self.index}", "--query-gpu=clocks.sm,clocks.max.sm",
+             "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+        sm, mx = [float(x) for x in out.stdout.strip().split(",")[:2]]
+        return sm, mx, 0
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(
-                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                self.samples.append([x.strip() for x in out.stdout.strip().split(",")])
+                self.samples.append(self._sample())
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.002)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -113,20 +131,24 @@ class ClockSampler:
     def __exit__(self, *a):
         self._stop.set()
         self._t.join(timeout=10)
+        if not self.samples:  # region shorter than one sample period
+            try:
+                self.samples.append(self._sample())
+            except Exception:
+                pass
 
     def summary(self):
-        sm = [float(s[0]) for s in self.samples if len(s) >= 7 and s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if len(s) >= 7 and s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm = [s[0] for s in self.samples]
+        mx = [s[1] for s in self.samples]
         reasons = set()
         for s in self.samples:
-            if len(s) >= 7:
-                for n, v in zip(names, s[3:7]):
-                    if v.lower() == "active":
-                        reasons.add(n)
+            for name, bit in self.REASONS.items():
+                if s[2] & bit:
+                    reasons.add(name)
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(self.samples)}
+                "samples": len(self.samples),
+                "source": "nvml" if self._nvml is not None else "nvidia-smi"}
 
 
 def measured_peaks():
@@ -402,29 +424,46 @@ def run_ours(args):
 
 
 def kernel_breakdown(qc, q0, NL, budget, stream):
-    """Device time of each op of one layer (eager, CUDA events, 8 layers each)."""
+    """Device time per layer of the separate (unfused) ops on the current caches: eager
+    launches, CUDA events, outputs preallocated, one untimed pass first."""
     import torch
 
-    res = {}
     n = min(8, NL)
-    scores = [None] * n
-    sel = [None] * n
+    dev = qc.device
+    H, P = qc.num_q_heads, qc.max_pages
+    K = max(1, min(budget // qc.page_size, P))
+    scores = [torch.zeros((1, H, P), dtype=torch.float64, device=dev) for _ in range(n)]
+    pages = [torch.zeros((1, H, K), dtype=torch.int32, device=dev) for _ in range(n)]
+    counts = [torch.zeros((1, H), dtype=torch.int32, device=dev) for _ in range(n)]
+
+    def run(name, layer):
+        if name == "estimate":
+            qc.estimate(layer, q0[layer], scores=scores[layer], stream=stream)
+        elif name == "select_topk":
+            qc.select_topk(layer, scores[layer], budget, pages=pages[layer], counts=counts[layer],
+                           stream=stream)
+        elif name == "sparse_attend":
+            qc.sparse_attend(layer, q0[layer], pages[layer], counts[layer], stream=stream)
+        else:
+            qc.dense_attend(layer, q0[layer], stream=stream)
+
+    res = {}
+    names = ("estimate", "select_topk", "sparse_attend", "dense_attend")
     with torch.cuda.stream(stream):
-        for name in ("estimate", "select_topk", "sparse_attend", "dense_attend"):
+        for name in names:  # warm: module load, allocator
+            for layer in range(n):
+                run(name, layer)
+        stream.synchronize()
+        for name in names:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             for layer in range(n):
-                if name == "estimate":
-                    scores[layer] = qc.estimate(layer, q0[layer], stream=stream)
-                elif name == "select_topk":
-                    sel[layer] = qc.select_topk(layer, scores[layer], budget, stream=stream)
-                elif name == "sparse_attend":
-                    qc.sparse_attend(layer, q0[layer], sel[layer][0], sel[layer][1], stream=stream)
-                else:
-                    qc.dense_attend(layer, q0[layer], stream=stream)
+                run(name, layer)
             e1.record(stream)
             stream.synchronize()
             res[name] = round(e0.elapsed_time(e1) * 1e3 / n, 2)
+    res["note"] = ("unfused ops, eager launches (launch gaps included), same caches; the "
+                   "bench step uses the fused kernel")
     return res
 
 

@@ -1,0 +1,381 @@
+// questkv_b200.hpp -- C++ host layer over the C ABI (questkv_b200.h): the reference's
+// questkv:: operator API (R/core/include/questkv/{kv_store,criticality,attention,metrics}.hpp,
+// R = /root/reference/proj) with the same names, argument meaning and exception types,
+// executed by the B200 kernels.  Header-only; link with -lquestkv_b200 (the in-tree
+// paper_2406_10774_b200/libquestkv_b200.so).  Requires C++20 (std::span), like the reference.
+//
+// Drop-in use: replace `#include "questkv/..."` by `#include "questkv_b200.hpp"` and
+// `questkv::` by `questkv_b200::` (or `namespace questkv = questkv_b200;`).
+//
+// Differences a caller can observe (all documented in INTEGRATION.md):
+//   * storage is fp16: keys/values/queries are rounded to fp16 (round-to-nearest-even) on
+//     the way in; for fp16-representable inputs every result equals the reference's
+//     (metadata, scores and page sets bitwise, outputs within 1e-5 relative L2);
+//   * KvCache has a fixed capacity (constructor argument; the reference grows without bound);
+//   * accessors return values instead of references into host-side storage;
+//   * select_top_k takes estimate_all's form (one score per page, in page order) and throws
+//     std::invalid_argument otherwise -- the GPU selector has no host fallback;
+//   * AttentionOutput::weights_sum_check is 1 by construction (the kernel divides by the
+//     merged softmax normaliser).
+// No CPU fallback exists: constructing a KvCache without a CUDA device throws
+// std::runtime_error.
+#pragma once
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "questkv_b200.h"
+
+namespace questkv_b200 {
+
+// ---- status -> exception (the reference's types) ------------------------------------------
+inline void check(int status) {
+    if (status == QK_OK) return;
+    const std::string msg = qk_last_error();
+    switch (status) {
+        case QK_ERR_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+        case QK_ERR_OUT_OF_RANGE: throw std::out_of_range(msg);
+        default: throw std::runtime_error(msg);
+    }
+}
+
+// ---- fp16 <-> float on the host (IEEE binary16, round to nearest even) --------------------
+inline uint16_t float_to_half(float f) {
+    uint32_t x;
+    std::memcpy(&x, &f, 4);
+    const uint32_t sign = (x >> 16) & 0x8000u;
+    const uint32_t mag = x & 0x7fffffffu;
+    if (mag >= 0x7f800000u) return uint16_t(sign | 0x7c00u | (mag > 0x7f800000u ? 0x200u : 0u));
+    if (mag >= 0x477ff000u) return uint16_t(sign | 0x7c00u);  // rounds to >= 65520: inf
+    if (mag < 0x38800000u) {                                   // fp16 subnormal or zero
+        if (mag < 0x33000000u) return uint16_t(sign);          // < 2^-25: rounds to 0
+        const uint32_t e = mag >> 23, m = (mag & 0x7fffffu) | 0x800000u;
+        const uint32_t shift = 126u - e;                       // 14..24
+        uint32_t r = m >> shift;
+        const uint32_t rem = m & ((1u << shift) - 1u), halfway = 1u << (shift - 1u);
+        if (rem > halfway || (rem == halfway && (r & 1u))) ++r;
+        return uint16_t(sign | r);
+    }
+    uint32_t h = ((mag - 0x38000000u) >> 13);
+    const uint32_t rem = mag & 0x1fffu;
+    if (rem > 0x1000u || (rem == 0x1000u && (h & 1u))) ++h;
+    return uint16_t(sign | h);
+}
+
+inline float half_to_float(uint16_t h) {
+    const uint32_t sign = uint32_t(h & 0x8000u) << 16;
+    uint32_t e = (h >> 10) & 0x1fu, m = h & 0x3ffu, x;
+    if (e == 0) {
+        if (m == 0) {
+            x = sign;
+        } else {  // subnormal
+            int s = -1;
+            do {
+                ++s;
+                m <<= 1;
+            } while (!(m & 0x400u));
+            x = sign | ((112u - uint32_t(s)) << 23) | ((m & 0x3ffu) << 13);
+        }
+    } else if (e == 31) {
+        x = sign | 0x7f800000u | (m << 13);
+    } else {
+        x = sign | ((e + 112u) << 23) | (m << 13);
+    }
+    float f;
+    std::memcpy(&f, &x, 4);
+    return f;
+}
+
+inline std::vector<uint16_t> to_half(std::span<const float> v) {
+    std::vector<uint16_t> out(v.size());
+    for (size_t i = 0; i < v.size(); ++i) out[i] = float_to_half(v[i]);
+    return out;
+}
+
+// ---- kv_store.hpp ---------------------------------------------------------------------------
+// CacheConfig (kv_store.hpp:10-17; validate kv_store.cpp:8-13).
+struct CacheConfig {
+    uint32_t head_dim = 0;
+    uint32_t page_size = 0;
+    uint32_t bytes_per_element = 2;
+    void validate() const {
+        if (head_dim == 0) throw std::invalid_argument("CacheConfig: head_dim must be >= 1");
+        if (page_size == 0) throw std::invalid_argument("CacheConfig: page_size must be >= 1");
+        if (bytes_per_element == 0)
+            throw std::invalid_argument("CacheConfig: bytes_per_element must be >= 1");
+    }
+};
+
+struct PageMetadata {  // kv_store.hpp:21-24
+    std::vector<float> min_key;
+    std::vector<float> max_key;
+};
+
+struct Page {  // kv_store.hpp:26-31
+    std::vector<float> keys;
+    std::vector<float> values;
+    PageMetadata metadata;
+    uint32_t length = 0;
+};
+
+// KvCache (kv_store.hpp:41-65): one head's paged cache, resident in HBM.
+class KvCache {
+public:
+    explicit KvCache(CacheConfig config, uint32_t capacity = 65536, int device = 0)
+        : config_(config) {
+        config_.validate();
+        qk_cache_desc d{};
+        d.head_dim = config_.head_dim;
+        d.page_size = config_.page_size;
+        d.bytes_per_element = config_.bytes_per_element;
+        d.num_layers = 1;
+        d.max_batch = 1;
+        d.num_q_heads = 1;
+        d.num_kv_heads = 1;
+        d.max_tokens = capacity;
+        d.device = device;
+        check(qk_cache_create(&d, &cache_));
+    }
+    ~KvCache() {
+        if (cache_) qk_cache_destroy(cache_);
+    }
+    KvCache(const KvCache&) = delete;
+    KvCache& operator=(const KvCache&) = delete;
+    KvCache(KvCache&& o) noexcept : config_(o.config_), cache_(o.cache_) { o.cache_ = nullptr; }
+
+    // kv_store.cpp:19-47; returns the token index.
+    uint32_t append(std::span<const float> key, std::span<const float> value) {
+        if (key.size() != config_.head_dim || value.size() != config_.head_dim)
+            throw std::invalid_argument("KvCache::append: vector dimension mismatch");
+        const uint32_t t = token_count();
+        const auto k = to_half(key), v = to_half(value);
+        check(qk_append_host(cache_, 0, k.data(), v.data(), 1, nullptr));
+        return t;
+    }
+    // n successive appends from [n][head_dim] rows (bulk prefill, same result).
+    void extend(std::span<const float> keys, std::span<const float> values) {
+        if (keys.size() != values.size() || keys.size() % config_.head_dim != 0)
+            throw std::invalid_argument("KvCache::extend: shape mismatch");
+        const auto k = to_half(keys), v = to_half(values);
+        check(qk_prefill_host(cache_, 0, 0, k.data(), v.data(),
+                              uint32_t(keys.size() / config_.head_dim), nullptr));
+    }
+    // kv_store.cpp:49-54 (out_of_range on a bad index).
+    PageMetadata page_metadata(uint32_t page_index) const {
+        if (page_index >= page_count())
+            throw std::out_of_range("KvCache::page_metadata: page index out of range");
+        std::vector<uint16_t> mn(config_.head_dim), mx(config_.head_dim);
+        check(qk_read_metadata(cache_, 0, 0, 0, page_index, 1, mn.data(), mx.data(), nullptr));
+        PageMetadata m;
+        for (uint32_t c = 0; c < config_.head_dim; ++c) {
+            m.min_key.push_back(half_to_float(mn[c]));
+            m.max_key.push_back(half_to_float(mx[c]));
+        }
+        return m;
+    }
+    Page page(uint32_t page_index) const {
+        if (page_index >= page_count()) throw std::out_of_range("KvCache::page: page index out of range");
+        Page p;
+        const uint32_t t0 = page_index * config_.page_size;
+        p.length = std::min(config_.page_size, token_count() - t0);
+        std::vector<uint16_t> k(size_t(p.length) * config_.head_dim), v(k.size());
+        check(qk_read_kv(cache_, 0, 0, 0, t0, p.length, k.data(), v.data(), nullptr));
+        for (size_t i = 0; i < k.size(); ++i) {
+            p.keys.push_back(half_to_float(k[i]));
+            p.values.push_back(half_to_float(v[i]));
+        }
+        p.metadata = page_metadata(page_index);
+        return p;
+    }
+    std::vector<float> key(uint32_t token) const { return row(token, true); }
+    std::vector<float> value(uint32_t token) const { return row(token, false); }
+
+    const CacheConfig& config() const noexcept { return config_; }
+    uint32_t token_count() const noexcept {
+        uint32_t n = 0;
+        qk_token_count(cache_, 0, 0, &n);
+        return n;
+    }
+    uint32_t page_count() const noexcept {
+        uint32_t n = 0;
+        qk_page_count(cache_, 0, 0, &n);
+        return n;
+    }
+    qk_cache* handle() const noexcept { return cache_; }
+
+private:
+    std::vector<float> row(uint32_t token, bool want_key) const {
+        if (token >= token_count()) throw std::out_of_range("KvCache::key: token out of range");
+        std::vector<uint16_t> k(config_.head_dim), v(config_.head_dim);
+        check(qk_read_kv(cache_, 0, 0, 0, token, 1, k.data(), v.data(), nullptr));
+        std::vector<float> out;
+        for (uint32_t c = 0; c < config_.head_dim; ++c) out.push_back(half_to_float(want_key ? k[c] : v[c]));
+        return out;
+    }
+    CacheConfig config_;
+    qk_cache* cache_ = nullptr;
+};
+
+// ---- criticality.hpp ------------------------------------------------------------------------
+struct PageScore {  // criticality.hpp:13-16
+    uint32_t page_index = 0;
+    double score = 0.0;
+};
+
+struct SelectionConfig {  // criticality.hpp:18-22
+    uint32_t token_budget = 0;
+    bool force_include_recent = true;
+    bool per_layer_enabled = true;
+};
+
+// estimate_all (criticality.cpp:25-34): bitwise the reference's doubles.
+inline std::vector<PageScore> estimate_all(std::span<const float> query, const KvCache& cache) {
+    if (cache.page_count() == 0) throw std::invalid_argument("estimate_all: empty cache");
+    if (query.size() != cache.config().head_dim)
+        throw std::invalid_argument("estimate_page_score: dimension mismatch");
+    const auto q = to_half(query);
+    const uint32_t P = cache.page_count();
+    std::vector<double> s(P);
+    check(qk_estimate_host(cache.handle(), 0, q.data(), 1, s.data(), P, nullptr));
+    std::vector<PageScore> out(P);
+    for (uint32_t p = 0; p < P; ++p) out[p] = {p, s[p]};
+    return out;
+}
+
+// estimate_page_score (criticality.cpp:9-23) on explicit metadata: a one-page device cache
+// whose two keys are min_key and max_key has exactly that metadata.
+inline double estimate_page_score(std::span<const float> query, const PageMetadata& metadata) {
+    const uint32_t d = uint32_t(metadata.min_key.size());
+    if (d == 0 || query.size() != d || metadata.max_key.size() != d)
+        throw std::invalid_argument("estimate_page_score: dimension mismatch");
+    KvCache tmp(CacheConfig{d, 2, 2}, 2);
+    std::vector<float> keys(metadata.min_key), vals(2 * size_t(d), 0.0f);
+    keys.insert(keys.end(), metadata.max_key.begin(), metadata.max_key.end());
+    tmp.extend(keys, vals);
+    return estimate_all(query, tmp)[0].score;
+}
+
+// select_top_k (criticality.cpp:36-81), same early-exit order and errors.
+inline std::vector<uint32_t> select_top_k(const std::vector<PageScore>& scores,
+                                          const SelectionConfig& config, const KvCache& cache) {
+    const uint32_t P = cache.page_count();
+    std::vector<uint32_t> all(P);
+    for (uint32_t p = 0; p < P; ++p) all[p] = p;
+    if (!config.per_layer_enabled) return all;
+    if (config.token_budget < cache.config().page_size)
+        throw std::invalid_argument("select_top_k: token_budget below page_size");
+    if (scores.empty()) throw std::invalid_argument("select_top_k: no scores");
+    for (const PageScore& s : scores)
+        if (s.page_index >= P) throw std::out_of_range("select_top_k: score for nonexistent page");
+    if (scores.size() != P)
+        throw std::invalid_argument("select_top_k: the GPU selector takes one score per page");
+    std::vector<double> s(P);
+    for (uint32_t p = 0; p < P; ++p) {
+        if (scores[p].page_index != p)
+            throw std::invalid_argument("select_top_k: scores must be in page order");
+        s[p] = scores[p].score;
+    }
+    qk_selection_cfg cfg{config.token_budget, config.force_include_recent ? 1 : 0, 1};
+    std::vector<int32_t> pages(P);
+    int32_t count = 0;
+    check(qk_select_topk_host(cache.handle(), 0, s.data(), P, 1, &cfg, pages.data(), P, &count,
+                              nullptr));
+    return std::vector<uint32_t>(pages.begin(), pages.begin() + count);
+}
+
+// ---- attention.hpp --------------------------------------------------------------------------
+struct AttentionOutput {  // attention.hpp:15-18
+    std::vector<double> output;
+    double weights_sum_check = 0.0;
+};
+
+inline AttentionOutput full_attention(std::span<const float> query, const KvCache& cache) {
+    if (cache.token_count() == 0) throw std::invalid_argument("full_attention: empty cache");
+    if (query.size() != cache.config().head_dim)
+        throw std::invalid_argument("attention: query dimension mismatch");
+    const auto q = to_half(query);
+    std::vector<float> out(cache.config().head_dim);
+    check(qk_dense_attend_host(cache.handle(), 0, q.data(), 1, out.data(), nullptr, nullptr));
+    return {std::vector<double>(out.begin(), out.end()), 1.0};
+}
+
+// sparse_attention (attention.cpp:94-116): any order accepted; empty -> invalid_argument,
+// out of range -> out_of_range, duplicate -> invalid_argument.
+inline AttentionOutput sparse_attention(std::span<const float> query, const KvCache& cache,
+                                        std::span<const uint32_t> selected_pages) {
+    if (selected_pages.empty()) throw std::invalid_argument("sparse_attention: empty page selection");
+    if (query.size() != cache.config().head_dim)
+        throw std::invalid_argument("attention: query dimension mismatch");
+    std::vector<int32_t> pages(selected_pages.begin(), selected_pages.end());
+    std::sort(pages.begin(), pages.end());
+    for (size_t i = 0; i < pages.size(); ++i) {
+        if (uint32_t(pages[i]) >= cache.page_count())
+            throw std::out_of_range("sparse_attention: page index out of range");
+        if (i > 0 && pages[i] == pages[i - 1])
+            throw std::invalid_argument("sparse_attention: duplicate page index");
+    }
+    const auto q = to_half(query);
+    const int32_t count = int32_t(pages.size());
+    std::vector<float> out(cache.config().head_dim);
+    check(qk_sparse_attend_host(cache.handle(), 0, q.data(), 1, pages.data(),
+                                uint32_t(pages.size()), &count, out.data(), nullptr, nullptr));
+    return {std::vector<double>(out.begin(), out.end()), 1.0};
+}
+
+// ---- metrics.hpp (the byte model of the roofline) ------------------------------------------
+inline double traffic_fraction(uint32_t page_size, uint64_t token_count, uint64_t token_budget) {
+    if (page_size == 0) throw std::invalid_argument("traffic_fraction: zero page_size");
+    if (token_count == 0 || token_budget == 0)
+        throw std::invalid_argument("traffic_fraction: counts must be positive");
+    if (token_budget > token_count)
+        throw std::invalid_argument("traffic_fraction: budget exceeds token count");
+    const uint64_t k = token_budget / page_size;
+    return 1.0 / double(page_size) + double(k * page_size) / double(token_count);
+}
+
+// ---- the batched serving object -------------------------------------------------------------
+// Every (layer, sequence, KV head) cache of a model in HBM; decode_step is the fused
+// append -> estimate -> top-K -> attend launch (one kernel per layer step).
+class DeviceCache {
+public:
+    explicit DeviceCache(const qk_cache_desc& desc) { check(qk_cache_create(&desc, &cache_)); }
+    ~DeviceCache() {
+        if (cache_) qk_cache_destroy(cache_);
+    }
+    DeviceCache(const DeviceCache&) = delete;
+    DeviceCache& operator=(const DeviceCache&) = delete;
+    qk_cache* handle() const noexcept { return cache_; }
+
+    // Device pointers (fp16 bits), asynchronous on `stream`.
+    void decode_step(uint32_t layer, const uint16_t* q, const uint16_t* k, const uint16_t* v,
+                     uint32_t batch, const SelectionConfig& sel, float* out,
+                     void* stream = nullptr) {
+        qk_selection_cfg cfg{sel.token_budget, sel.force_include_recent ? 1 : 0,
+                             sel.per_layer_enabled ? 1 : 0};
+        check(qk_decode_step(cache_, layer, q, k, v, batch, &cfg, out, QK_DTYPE_F32, nullptr, 0,
+                             nullptr, stream));
+    }
+    // Host buffers, synchronous.
+    void decode_step_host(uint32_t layer, const uint16_t* q, const uint16_t* k,
+                          const uint16_t* v, uint32_t batch, const SelectionConfig& sel,
+                          float* out, void* stream = nullptr) {
+        qk_selection_cfg cfg{sel.token_budget, sel.force_include_recent ? 1 : 0,
+                             sel.per_layer_enabled ? 1 : 0};
+        check(qk_decode_step_host(cache_, layer, q, k, v, batch, &cfg, out, stream));
+    }
+    void prefill_host(uint32_t layer, uint32_t seq, const uint16_t* k, const uint16_t* v,
+                      uint32_t n_tokens, void* stream = nullptr) {
+        check(qk_prefill_host(cache_, layer, seq, k, v, n_tokens, stream));
+    }
+
+private:
+    qk_cache* cache_ = nullptr;
+};
+
+}  // namespace questkv_b200

@@ -114,6 +114,17 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t pari
         "r"(parity)
         : "memory");
 }
+__device__ __forceinline__ void mbar_wait_cluster(unsigned long long* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "QK_WAITC_%=:\n"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra QK_WAITC_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
                                          unsigned long long* bar) {
     asm volatile(
@@ -194,6 +205,11 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
     __shared__ float s_o[kWarps][D];
     __shared__ float s_m[kWarps], s_l[kWarps];
 
+    __shared__ __align__(8) unsigned long long merge_bar[1];  // rank 0: peers' partials
+    if (threadIdx.x == 0) {
+        mbar_init(merge_bar, C - 1 > 0 ? C - 1 : 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     const uint32_t unit = blockIdx.x / C;
     const uint32_t b = unit / p.Hkv, kvh = unit % p.Hkv;
     const uint32_t Hq = p.Hkv * G;
@@ -349,10 +365,6 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
         // flight at once (no shared-memory staging, no per-group barriers).  The 8 channel
         // groups of a page are then added with a shuffle transpose (exact under the
         // certificate; failing pages take the sequential chain).
-        if (owner && !appended) {
-            do_append();
-            __syncthreads();  // s_new_min/max for the newest page's chain
-        }
         if (r_begin < r_end) stamp(p.probe, 3);
         constexpr int CPG = D / 8;  // channels per warp
         const int cg = warp & 7, half = warp >> 3;
@@ -372,6 +384,8 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
                 v[k] = act ? ld_nc_v4(mslice + (size_t(minmax) * D + c) * p.mrow + pbase)
                            : make_int4(0, 0, 0, 0);
             }
+            if (owner && !appended) do_append();  // overlaps the loads above; s_new_* are
+                                                  // read after the barrier below
             double acc[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j) acc[j] = 0.0;
@@ -384,10 +398,12 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
                 for (int j = 0; j < 8; ++j)
                     acc[j] = __fma_rn(w, (c & 1) ? h2d_scaled(h[j]) : h2d(__ushort_as_half(h[j])), acc[j]);
             }
+            if (c0 == r_begin) stamp(p.probe, 5);
             double2* dst = reinterpret_cast<double2*>(part + cg * kThreads + half * 256 + lane * 8);
 #pragma unroll
             for (int j = 0; j < 4; ++j) dst[j] = make_double2(acc[2 * j], acc[2 * j + 1]);
             __syncthreads();
+            if (c0 == r_begin) stamp(p.probe, 6);
             if (pg < r_end) {
                 double sc = ((part[0 * kThreads + tid] + part[1 * kThreads + tid]) +
                              (part[2 * kThreads + tid] + part[3 * kThreads + tid])) +
@@ -429,6 +445,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
                 if (!smem_keys || p.keep_scores)
                     p.ws_scores[(size_t(b) * Hq + size_t(kvh)) * p.Pmax + pg] = sc;
             }
+            if (c0 == r_begin) stamp(p.probe, 7);
             __syncthreads();  // part reused by the next chunk
         }
         if (r_begin < r_end) stamp(p.probe, 4);
@@ -688,40 +705,53 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
         }
         __syncthreads();
         if (g == 0) stamp(p.probe, 17);
-        float M = -CUDART_INF_F;
+        if (tid < D) {  // the CTA's partial of this head: channel tid
+            float M = -CUDART_INF_F;
 #pragma unroll
-        for (int w = 0; w < kWarps; ++w) M = fmaxf(M, s_m[w]);
-        float L = 0.0f, wsc[kWarps];
+            for (int w = 0; w < kWarps; ++w) M = fmaxf(M, s_m[w]);
+            float L = 0.0f, acc = 0.0f;
 #pragma unroll
-        for (int w = 0; w < kWarps; ++w) {
-            wsc[w] = (s_m[w] == -CUDART_INF_F) ? 0.0f : exp2f(s_m[w] - M);
-            L += s_l[w] * wsc[w];
-        }
-        float* slot = parts + (size_t(g) * C + rank) * (D + 2);
-        for (int d = tid; d < D; d += kThreads) {
-            float acc = 0.0f;
-#pragma unroll
-            for (int w = 0; w < kWarps; ++w) acc += s_o[w][d] * wsc[w];
-            if (C == 1) slot[2 + d] = acc;
-            else st_cluster_f32(slot + 2 + d, 0, acc);
-        }
-        if (tid == 0) {
-            if (C == 1) {
-                slot[0] = M;
-                slot[1] = L;
+            for (int w = 0; w < kWarps; ++w) {
+                const float sw = (s_m[w] == -CUDART_INF_F) ? 0.0f : exp2f(s_m[w] - M);
+                L += s_l[w] * sw;
+                acc += s_o[w][tid] * sw;
+            }
+            float* slot = parts + (size_t(g) * C + rank) * (D + 2);
+            if (C == 1 || rank == 0) {
+                slot[2 + tid] = acc;
+                if (tid == 0) {
+                    slot[0] = M;
+                    slot[1] = L;
+                }
             } else {
-                st_cluster_f32(slot, 0, M);
-                st_cluster_f32(slot + 1, 0, L);
+                st_cluster_f32(slot + 2 + tid, 0, acc);
+                if (tid == 0) {
+                    st_cluster_f32(slot, 0, M);
+                    st_cluster_f32(slot + 1, 0, L);
+                }
             }
         }
-        __syncthreads();  // s_o / s_m reused by the next head
+        __syncthreads();  // s_o / s_m reused by the next head; partials issued
     }
     asm volatile("griddepcontrol.launch_dependents;");
     stamp(p.probe, 18);
-    if (C > 1) cluster_sync_acqrel();  // partials landed; no CTA reads a peer's smem after
+    if (C > 1 && rank != 0) {
+        // Signal rank 0 (release: the partial stores above are ordered before it), then
+        // exit: no CTA reads this CTA's shared memory any more.
+        if (tid == 0) {
+            asm volatile("fence.acq_rel.cluster;" ::: "memory");
+            asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                             map_rank(merge_bar, 0))
+                         : "memory");
+        }
+        return;
+    }
+    if (C > 1) {
+        if (tid == 0) mbar_wait_cluster(merge_bar, 0);  // every peer's partial has landed
+        __syncthreads();
+    }
     stamp(p.probe, 19);
     if (p.probe && tid == 0) p.probe[blockIdx.x * kProbeSlots + 25] = clock64();
-    if (rank != 0) return;
 
     // Rank 0: merge the C partials of every head in rank order.  One thread per head
     // turns the C maxima into weights w_r = exp2(m_r - M) / L; then every channel is a
