@@ -232,7 +232,8 @@ QK_API int qk_sync_lengths(qk_cache *cache, void *stream);
 QK_API int qk_check_status(qk_cache *cache, void *stream);
 
 /* Diagnostics: with QK_PROBE=1 in the environment at qk_cache_create, the fused decode
- * kernel records up to 32 %globaltimer stamps per CTA at its phase boundaries (see
+ * kernel records up to 32 %globaltimer stamps per CTA at its phase boundaries, one record per
+ * layer ([layer][max_batch*num_kv_heads*16][32] u64; see
  * decode.cu; tools/probe_fused.py prints the timeline).  Copies the first n and clears
  * the record (synchronous). */
 QK_API int qk_debug_probe(qk_cache *cache, uint64_t *host, uint32_t n, void *stream);

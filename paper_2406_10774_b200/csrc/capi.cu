@@ -158,7 +158,7 @@ int qk_cache_create(const qk_cache_desc* desc, qk_cache** out) {
     if (!rc) rc = dmalloc(c, &c->ws_ticket, size_t(c->B) * c->Hq);
     if (!rc) rc = dmalloc(c, &c->d_status, 1);
     if (!rc) rc = dmalloc(c, &c->len_ticket, size_t(c->L) * c->B);
-    if (!rc && getenv("QK_PROBE")) rc = dmalloc(c, &c->probe, size_t(c->B) * c->Hkv * kMaxClusterCtas * kProbeSlots);
+    if (!rc && getenv("QK_PROBE")) rc = dmalloc(c, &c->probe, size_t(c->L) * c->B * c->Hkv * kMaxClusterCtas * kProbeSlots);
     if (!rc) rc = dmalloc(c, &c->ws_scores, size_t(c->B) * c->Hq * c->Pmax);
     if (!rc) rc = dmalloc(c, &c->ws_pages, size_t(c->B) * c->Hq * c->Pmax);
     if (!rc) rc = dmalloc(c, &c->ws_counts, size_t(c->B) * c->Hq);
@@ -677,7 +677,7 @@ int qk_dense_attend_host(const qk_cache* cc, uint32_t layer, const uint16_t* q_h
 int qk_debug_probe(qk_cache* c, uint64_t* host, uint32_t n, void* stream) {
     if (!c || !host) return set_error(QK_ERR_INVALID_ARGUMENT, "qk_debug_probe: null argument");
     if (!c->probe) return set_error(QK_ERR_INVALID_ARGUMENT, "qk_debug_probe: set QK_PROBE=1 before qk_cache_create");
-    const size_t cap = size_t(c->B) * c->Hkv * kMaxClusterCtas * kProbeSlots;
+    const size_t cap = size_t(c->L) * c->B * c->Hkv * kMaxClusterCtas * kProbeSlots;
     const size_t cnt = n < cap ? n : cap;
     DeviceGuard guard(c->desc.device);
     cudaStream_t st = as_stream(stream);

@@ -23,6 +23,8 @@
 // restores the full estimate_all (every page, scores kept in HBM) for parity tests.
 // The launch uses programmatic dependent launch; griddepcontrol.wait precedes every read
 // of data a prior kernel wrote.
+#include <type_traits>
+
 #include "attend_warp.cuh"
 #include "select.cuh"
 
@@ -359,23 +361,80 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
     asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
     stamp(p.probe, 22);
     if constexpr (G == 1) {
-        // MHA: metadata straight into registers.  Lane (pb, cg) of warp w owns pages
-        // base + 8*pb .. +7 (base = c0 + 32w) over channels [cg*CPG, cg*CPG + CPG): one
-        // 16-byte load per channel of its sign-selected row; every warp keeps its loads in
-        // flight at once (no shared-memory staging, no per-group barriers).  The 8 channel
-        // groups of a page are then added with a shuffle transpose (exact under the
-        // certificate; failing pages take the sequential chain).
-        if (r_begin < r_end) stamp(p.probe, 3);
+        // MHA: metadata straight into registers.  Warp (half, cg) covers pages
+        // c0 + 256*half + 8*lane .. +7 over channels [cg*CPG, cg*CPG + CPG): one 16-byte
+        // load per channel of its sign-selected row, every load instruction 512 contiguous
+        // bytes, all of a pass in flight at once.  The 8 channel-group partial sums of a
+        // page are added through shared memory (exact under the certificate; failing pages
+        // take the sequential chain).  A remainder of <= kTail pages past the 512-page
+        // passes is staged with cp.async at the start and finished after the last pass, so
+        // it costs no extra round trip.
         constexpr int CPG = D / 8;  // channels per warp
+        constexpr uint32_t kTail = 64;
         const int cg = warp & 7, half = warp >> 3;
-        double* part = reinterpret_cast<double*>(smem);  // [8][512] partial sums (region A)
-        for (uint32_t c0 = r_begin; c0 < r_end; c0 += kThreads) {
-            // Warp (half, cg): pages c0 + 256*half + 8*lane .. +7, channels cg*CPG + [0, CPG):
-            // every load instruction reads 512 contiguous bytes of one metadata row.
+        double* part = reinterpret_cast<double*>(smem);               // [8][512] (region A)
+        __half* tstage = reinterpret_cast<__half*>(part + 8 * kThreads);  // [D][kTail]
+        const uint32_t n_mine = r_end - r_begin;
+        const uint32_t rem = n_mine % kThreads;
+        const uint32_t tail = (n_mine > kThreads && rem != 0 && rem <= kTail) ? rem : 0u;
+        const uint32_t main_end = r_end - tail;
+        if (tail) {
+            const int pieces = int((tail + 7) / 8);
+            for (int i = tid; i < D * pieces; i += kThreads) {
+                const int c = i / pieces, pc = i % pieces;
+                const int minmax = (need[c] & 2) ? 0 : 1;
+                cp_async16(tstage + size_t(c) * kTail + pc * 8,
+                           mslice + (size_t(minmax) * D + c) * p.mrow + main_end + pc * 8);
+            }
+            cp_async_commit();
+        }
+        const uint32_t tail_rec = (tid < int(tail)) ? __ldg(rslice + main_end + tid) : 0u;
+        if (r_begin < r_end) stamp(p.probe, 3);
+
+        // The certificate, the sequential fallback and the hand-off of one page's score.
+        auto finish = [&](uint32_t pg, double sc, uint32_t rec) {
+            const uint32_t xcode = rec >> 16, qcode = s_qcode[0];
+            bool exact = xcode >= 31u || qcode >= 31u;
+            if (!exact) {
+                const double bound = __dmul_ru(
+                    s_qabs[0], double(__half2float(__ushort_as_half(uint16_t(rec & 0x7fffu)))));
+                const int e = 5 + int(qcode) + int(xcode);
+                exact = bound < __longlong_as_double(static_cast<long long>(e + 1023) << 52);
+            }
+            const bool newest = patch && pg == new_page;
+            if (!exact || newest) {
+                if (p.probe) atomicAdd(p.probe + blockIdx.x * kProbeSlots + 23, 1ull);
+                // The reference's sequential chain (criticality.cpp:16-21).
+                double a = 0.0;
+                for (int c = 0; c < D; ++c) {
+                    const int minmax = (need[c] & 2) ? 0 : 1;
+                    const __half x = newest ? (minmax == 0 ? s_new_min[c] : s_new_max[c])
+                                            : mslice[(size_t(minmax) * D + c) * p.mrow + pg];
+                    const double w = (c & 1) ? dq[c] * 0x1p-1008 : dq[c];
+                    a = __fma_rn(w, h2d(x), a);
+                }
+                sc = a;
+            }
+            if (smem_keys) {
+                if (pg < n_cand) {
+                    const unsigned long long k = order_key(sc);
+                    const uint32_t a = smem_u32(keys + key_slot(pg));
+                    for (uint32_t r = 0; r < C; ++r) {
+                        uint32_t ra;
+                        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(r));
+                        st_cluster_u64(ra, k);
+                    }
+                }
+            }
+            if (!smem_keys || p.keep_scores)
+                p.ws_scores[(size_t(b) * Hq + size_t(kvh)) * p.Pmax + pg] = sc;
+        };
+
+        for (uint32_t c0 = r_begin; c0 < main_end; c0 += kThreads) {
             const uint32_t pbase = c0 + uint32_t(half) * 256 + uint32_t(lane) * 8;
-            const bool act = pbase < r_end;  // pages past r_end are loaded (in-bounds) but unused
+            const bool act = pbase < main_end;  // pages past main_end: loaded in-bounds, unused
             const uint32_t pg = c0 + uint32_t(tid);  // the page this thread finishes below
-            const uint32_t rec = pg < r_end ? __ldg(rslice + pg) : 0u;  // issued with the rows
+            const uint32_t rec = pg < main_end ? __ldg(rslice + pg) : 0u;  // with the rows
             int4 v[CPG];
 #pragma unroll
             for (int k = 0; k < CPG; ++k) {
@@ -404,49 +463,37 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
             for (int j = 0; j < 4; ++j) dst[j] = make_double2(acc[2 * j], acc[2 * j + 1]);
             __syncthreads();
             if (c0 == r_begin) stamp(p.probe, 6);
-            if (pg < r_end) {
-                double sc = ((part[0 * kThreads + tid] + part[1 * kThreads + tid]) +
-                             (part[2 * kThreads + tid] + part[3 * kThreads + tid])) +
-                            ((part[4 * kThreads + tid] + part[5 * kThreads + tid]) +
-                             (part[6 * kThreads + tid] + part[7 * kThreads + tid]));
-                const uint32_t xcode = rec >> 16, qcode = s_qcode[0];
-                bool exact = xcode >= 31u || qcode >= 31u;
-                if (!exact) {
-                    const double bound = __dmul_ru(
-                        s_qabs[0], double(__half2float(__ushort_as_half(uint16_t(rec & 0x7fffu)))));
-                    const int e = 5 + int(qcode) + int(xcode);
-                    exact = bound < __longlong_as_double(static_cast<long long>(e + 1023) << 52);
-                }
-                const bool newest = patch && pg == new_page;
-                if (!exact || newest) {
-                    if (p.probe) atomicAdd(p.probe + blockIdx.x * kProbeSlots + 23, 1ull);
-                    // The reference's sequential chain (criticality.cpp:16-21).
-                    double a = 0.0;
-                    for (int c = 0; c < D; ++c) {
-                        const int minmax = (need[c] & 2) ? 0 : 1;
-                        const __half x = newest ? (minmax == 0 ? s_new_min[c] : s_new_max[c])
-                                                : mslice[(size_t(minmax) * D + c) * p.mrow + pg];
-                        const double w = (c & 1) ? dq[c] * 0x1p-1008 : dq[c];
-                        a = __fma_rn(w, h2d(x), a);
-                    }
-                    sc = a;
-                }
-                if (smem_keys) {
-                    if (pg < n_cand) {
-                        const unsigned long long k = order_key(sc);
-                        const uint32_t a = smem_u32(keys + key_slot(pg));
-                        for (uint32_t r = 0; r < C; ++r) {
-                            uint32_t ra;
-                            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(r));
-                            st_cluster_u64(ra, k);
-                        }
-                    }
-                }
-                if (!smem_keys || p.keep_scores)
-                    p.ws_scores[(size_t(b) * Hq + size_t(kvh)) * p.Pmax + pg] = sc;
+            if (pg < main_end) {
+                const double sc = ((part[0 * kThreads + tid] + part[1 * kThreads + tid]) +
+                                   (part[2 * kThreads + tid] + part[3 * kThreads + tid])) +
+                                  ((part[4 * kThreads + tid] + part[5 * kThreads + tid]) +
+                                   (part[6 * kThreads + tid] + part[7 * kThreads + tid]));
+                finish(pg, sc, rec);
             }
             if (c0 == r_begin) stamp(p.probe, 7);
-            __syncthreads();  // part reused by the next chunk
+            __syncthreads();  // part reused by the next pass
+        }
+        if (tail) {
+            if (owner && !appended) {
+                do_append();
+                __syncthreads();
+            }
+            cp_async_wait<0>();
+            __syncthreads();
+            if (uint32_t(tid) < tail) {
+                const uint32_t pg = main_end + tid;
+                double acc[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+                const unsigned short* t16 = reinterpret_cast<const unsigned short*>(tstage);
+#pragma unroll 16
+                for (int c = 0; c < D; ++c) {
+                    const unsigned short hh = t16[size_t(c) * kTail + tid];
+                    acc[c & 7] = __fma_rn(dq[c], (c & 1) ? h2d_scaled(hh) : h2d(__ushort_as_half(hh)), acc[c & 7]);
+                }
+                const double sc = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+                finish(pg, sc, tail_rec);
+            }
         }
         if (r_begin < r_end) stamp(p.probe, 4);
     } else {
@@ -612,10 +659,42 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
     if (!all_pages) {
         const uint32_t target = p.force ? p.k_budget - 1 : p.k_budget;
         if (target > 0) {
-            if (smem_keys && n_cand <= uint32_t(kSelThreads * kSelKpt)) {
-                // Groups of 128 threads, one head each (GQA heads in parallel).
-                const int grpi = warp / (kSelThreads / 32), gt = tid % kSelThreads;
-                for (int g = grpi; g < G; g += kSelGroups) {
+            // Groups of NTS threads select one head each (GQA heads in parallel); during an
+            // MHA selection the other warps prefetch into L2 the K/V pages the first radix
+            // pass proves selected (pages i % C == rank: the cluster requests each once),
+            // so HBM streams attention bytes while the boundary is still being resolved.
+            auto group_select = [&](auto nts_tag) {
+                constexpr int NTS = decltype(nts_tag)::value;
+                constexpr int NGRP = kThreads / NTS;
+                auto* gsc = reinterpret_cast<SelectScratch<NTS>*>(smem);  // region A
+                const int grpi = tid / NTS, gt = tid % NTS;
+                if (G == 1 && grpi > 0) {
+                    asm volatile("bar.sync %0, %1;" ::"r"(7), "r"(kThreads) : "memory");
+                    const bool ok = gsc[0].sig_valid != 0;
+                    const int shift = gsc[0].sig_shift;
+                    const unsigned int bin = gsc[0].sig_bin;
+                    const uint32_t page_bytes = p.S * D * 2;
+                    const __half* kslice0 = p.k_pool + s * p.slice_kv;
+                    const __half* vslice0 = p.v_pool + s * p.slice_kv;
+                    for (uint32_t i = rank + C * uint32_t(tid - NTS); i <= n_cand;
+                         i += C * uint32_t(kThreads - NTS)) {
+                        bool take;
+                        uint32_t pg = i;
+                        if (i == n_cand) {
+                            take = p.force != 0;  // the newest page
+                            pg = P - 1;
+                        } else {
+                            const unsigned long long k = keys[key_slot(i)];
+                            take = ok && unsigned(((k << shift) >> 32) >> 21) > bin;
+                        }
+                        if (!take) continue;
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(kslice0 + size_t(pg) * p.S * D),
+                                     "r"(page_bytes) : "memory");
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(vslice0 + size_t(pg) * p.S * D),
+                                     "r"(page_bytes) : "memory");
+                    }
+                }
+                for (int g = grpi; g < G; g += NGRP) {
                     const unsigned long long* kg = keys + size_t(g) * p.key_cap;
                     unsigned long long k16[kSelKpt];
                     const ulonglong2* src = reinterpret_cast<const ulonglong2*>(kg + key_slot(uint32_t(gt) * kSelKpt));
@@ -627,11 +706,17 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
                         k16[2 * j + 1] = v.y;
                     }
                     if (g == 0) stamp(p.probe, 10);
-                    block_select_reg<kSelThreads, kSelKpt>(k16, n_cand, target, kg[0],
-                                                           sel + g * kMaxFusedK, grp_sc[grpi], gt,
-                                                           1 + grpi, g == 0 ? p.probe : nullptr);
-                    group_sync<kSelThreads>(1 + grpi);  // scratch reuse for the next head
+                    block_select_reg<NTS, kSelKpt>(k16, n_cand, target, kg[0], sel + g * kMaxFusedK,
+                                                   gsc[grpi], gt, 1 + grpi,
+                                                   g == 0 ? p.probe : nullptr, G == 1 ? 7 : -1,
+                                                   kThreads);
+                    group_sync<NTS>(1 + grpi);  // scratch reuse for the next head
                 }
+            };
+            if (smem_keys && n_cand <= uint32_t(kSelThreads * kSelKpt)) {
+                group_select(std::integral_constant<int, kSelThreads>{});
+            } else if (smem_keys && n_cand <= uint32_t(2 * kSelThreads * kSelKpt)) {
+                group_select(std::integral_constant<int, 2 * kSelThreads>{});
             } else if (smem_keys && n_cand <= uint32_t(kThreads * kSelKpt)) {
                 for (int g = 0; g < G; ++g) {
                     const unsigned long long* kg = keys + size_t(g) * p.key_cap;
@@ -825,7 +910,7 @@ int run_fused(qk_cache* c, FusedParams prm, uint32_t batch, uint32_t cluster,
     attrs[0].val.clusterDim.y = 1;
     attrs[0].val.clusterDim.z = 1;
     attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attrs[1].val.programmaticStreamSerializationAllowed = 1;
+    attrs[1].val.programmaticStreamSerializationAllowed = getenv("QK_NO_PDL") ? 0 : 1;
     cfg.attrs = attrs;
     cfg.numAttrs = 2;
     const int rc = cuda_check(cudaLaunchKernelEx(&cfg, kern, prm, uint32_t(region_a)),
@@ -921,7 +1006,7 @@ int launch_decode(qk_cache* c, uint32_t layer, const __half* q, const __half* k,
     prm.out_dtype = out_dtype;
     prm.keep_scores = c->keep_scores ? 1 : 0;
     prm.scale_log2 = float(1.4426950408889634 / sqrt(double(c->desc.head_dim)));
-    prm.probe = c->probe;
+    prm.probe = c->probe ? c->probe + size_t(layer) * c->B * c->Hkv * kMaxClusterCtas * kProbeSlots : nullptr;
     const uint32_t cluster = fused_cluster_size(c, batch, max_pages);
     switch (c->D) {
         case 64: return dispatch_g<64>(c, prm, batch, cluster, max_pages, st);

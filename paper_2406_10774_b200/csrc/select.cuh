@@ -41,6 +41,11 @@ struct SelectScratch {
     unsigned int cand_idx[32];
     alignas(16) unsigned long long cand2[64];  // (key, index) pairs of the threshold bin
     unsigned int cand_take[32];
+    // Early-signal of block_select_reg: after the first radix pass every key whose top
+    // 11 bits (after the common prefix `sig_shift`) exceed `sig_bin` is selected.
+    int sig_shift;
+    unsigned int sig_bin;
+    int sig_valid;
     unsigned int n_cand;
     unsigned int digit, above, count;
     unsigned long long t_key;
@@ -538,10 +543,24 @@ __device__ void block_select_reg_wide(const unsigned long long (&key)[KPT], uint
 // verdicts then work on the high 32-bit word (one instruction per comparison instead of a
 // 64-bit mask-and-compare).  A pass that leaves more than 32 keys of the threshold bin
 // undecided (heavy ties) restarts in block_select_reg_wide.  Same contract.
+// `signal_bar` >= 0: after the first pass (or on the way to the wide path) thread 0 of the
+// group publishes (sig_shift, sig_bin, sig_valid) and the group arrives once on named
+// barrier `signal_bar` with `signal_count` threads, so other warps can start work on the
+// certainly-selected keys (the fused kernel prefetches their K/V pages).
 template <int NT, int KPT, typename OutT>
 __device__ void block_select_reg(const unsigned long long (&key)[KPT], uint32_t n, uint32_t target,
                                  unsigned long long ref, OutT* out, SelectScratch<NT>& sc, int gt,
-                                 int bar, unsigned long long* probe = nullptr) {
+                                 int bar, unsigned long long* probe = nullptr,
+                                 int signal_bar = -1, int signal_count = 0) {
+    auto signal = [&](int valid, int shift, unsigned int bin) {
+        if (signal_bar < 0) return;
+        if (gt == 0) {
+            sc.sig_shift = shift;
+            sc.sig_bin = bin;
+            sc.sig_valid = valid;
+        }
+        asm volatile("bar.arrive %0, %1;" ::"r"(signal_bar), "r"(signal_count) : "memory");
+    };
     constexpr int NW = NT / 32;
     constexpr int BPL = 2048 / NT;
     static_assert(NW % 4 == 0 && NW <= 32 && BPL % 4 == 0, "geometry");
@@ -571,6 +590,7 @@ __device__ void block_select_reg(const unsigned long long (&key)[KPT], uint32_t 
     }
     if (diff == 0) {  // every key equal: the lowest indices
         group_sync<NT>(bar);  // red_max read by all before the wide path reuses sc
+        signal(0, 0, 0);
         block_select_reg_wide<NT, KPT>(key, n, target, ref, out, sc, gt, bar, probe);
         return;
     }
@@ -614,6 +634,7 @@ __device__ void block_select_reg(const unsigned long long (&key)[KPT], uint32_t 
     const unsigned int bin = sc.digit, bin_count = sc.count;
     const unsigned int krem = target - sc.above;
     sel_stamp(probe, 11);
+    signal(1, shift, bin);  // keys of digit > bin are selected whatever happens next
     if (bin_count != krem && bin_count > 32) {  // needs more digits: the 64-bit path
         group_sync<NT>(bar);
         block_select_reg_wide<NT, KPT>(key, n, target, ref, out, sc, gt, bar, probe);

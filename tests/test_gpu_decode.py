@@ -90,6 +90,9 @@ class Layer:
     (2, 4, 2, 64, [1500, 33], 128),       # head_dim 64, GQA 2
     (1, 2, 2, 128, [40000], 4096),        # long context, cluster of 8, K = 256
     (1, 4, 4, 100, [700], 64),            # padded head_dim
+    (1, 4, 4, 128, [32800], 2048),        # 2051 pages: per-CTA tail pass, 256-thread select
+    (1, 4, 4, 128, [65000], 2048),        # 4063 pages: two estimate passes per CTA
+    (1, 2, 2, 128, [70000], 2048),        # 4375 pages: the 512-thread select
 ])
 @pytest.mark.parametrize("keep", [True, False])
 def test_fused_step_vs_oracle(qk, oracle_c, B, Hq, Hkv, d, lens, budget, keep):

@@ -41,8 +41,8 @@ kn = (torch.randn((args.batch, Hkv, D), generator=g, device=dev) / D ** 0.5).hal
 out = torch.empty((args.batch, H, D), dtype=torch.float32, device=dev)
 torch.cuda.synchronize()
 SLOTS = 32
-n = args.batch * Hkv * 16 * SLOTS
-buf = np.zeros(n, dtype=np.uint64)
+n = args.batch * Hkv * 16 * SLOTS      # one layer's record
+buf = np.zeros(n * args.layers, dtype=np.uint64)
 lib = _lib.load()
 names = {0: "entry", 1: "dep_wait", 2: "prologue", 21: "pre_cwait", 22: "cluster_wait", 3: "loads_issued", 5: "w0_computed", 6: "partials_synced", 7: "pushed", 4: "est_loop_end", 8: "estimate_end", 9: "barrier1", 10: "keys_pulled",
          11: "sel_pass0", 12: "sel_pass1", 13: "sel_pass2", 14: "sel_pair", 15: "sel_compact",
@@ -51,14 +51,14 @@ for _ in range(50):  # clocks up
     for layer in range(args.layers):
         qc.decode_step(layer, q, None, None, args.budget, out=out)
 torch.cuda.synchronize()
-lib.qk_debug_probe(qc._h, buf.ctypes.data, n, None)
+lib.qk_debug_probe(qc._h, buf.ctypes.data, buf.size, None)
 res = []
 for rep in range(args.reps):
     for layer in range(args.layers):
         qc.decode_step(layer, q, kn, kn, args.budget, out=out)
         torch.cuda.synchronize()
-        lib.qk_debug_probe(qc._h, buf.ctypes.data, n, None)
-        t = buf.reshape(-1, SLOTS).astype(np.int64)
+        lib.qk_debug_probe(qc._h, buf.ctypes.data, buf.size, None)
+        t = buf[layer * n:(layer + 1) * n].reshape(-1, SLOTS).astype(np.int64)
         t = t[t[:, 0] > 0]
         t0 = t[:, 0].min()
         fb = int(t[:, 23].sum())
@@ -79,3 +79,35 @@ for rep in range(args.reps):
         res.append(row)
 for r in res[-args.layers:]:
     print(json.dumps(r))
+
+# ---- graph mode: inter-kernel gaps of a CUDA graph of every layer (as bench.py runs) ----
+if os.environ.get("QK_PROBE_GRAPH"):
+    s = torch.cuda.Stream()
+    qb, kb = q.clone(), kn.clone()
+    g2 = torch.cuda.CUDAGraph()
+    qc.decode_step(0, qb, kb, kb, args.budget, out=out, stream=s)  # warm
+    s.synchronize()
+    with torch.cuda.graph(g2, stream=s):
+        for layer in range(args.layers):
+            qc.decode_step(layer, qb, kb, kb, args.budget, out=out, stream=s)
+    for _ in range(3):
+        g2.replay()
+    s.synchronize()
+    lib.qk_debug_probe(qc._h, buf.ctypes.data, buf.size, None)  # clear
+    big = np.zeros(n * args.layers, dtype=np.uint64)
+    g2.replay()
+    s.synchronize()
+    lib.qk_debug_probe(qc._h, big.ctypes.data, big.size, None)
+    per = big.reshape(args.layers, -1, SLOTS).astype(np.int64)
+    prev_end = None
+    for layer in range(args.layers):
+        t = per[layer]
+        t = t[t[:, 0] > 0]
+        start = t[:, 0].min()
+        ends = t[:, 1:23].max(axis=1)
+        end = ends.max()
+        gap = (start - prev_end) / 1000.0 if prev_end is not None else 0.0
+        print(json.dumps({"layer": layer, "kernel_us": round((end - start) / 1000.0, 2),
+                          "gap_from_prev_us": round(gap, 2),
+                          "entry_spread_us": round((t[:, 0].max() - start) / 1000.0, 2)}))
+        prev_end = end
