@@ -157,6 +157,7 @@ struct FusedParams {
     uint32_t k_budget;    // pages per query head (UINT32_MAX: selection disabled)
     uint32_t key_cap;     // key slots per head in the cluster-exchanged key array (0: HBM)
     int force, out_dtype, keep_scores;
+    int prefetch;         // L2-prefetch certainly-selected pages during the selection
     float scale_log2;
     unsigned long long* probe;  // optional [grid][kProbeSlots] globaltimer stamps
 };
@@ -445,6 +446,26 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
             }
             if (owner && !appended) do_append();  // overlaps the loads above; s_new_* are
                                                   // read after the barrier below
+            if (tail && c0 == r_begin) {
+                // The staged tail pages (issued first) are finished while this pass's
+                // register loads are still in flight.
+                cp_async_wait<0>();
+                __syncthreads();  // tail rows and s_new_* visible
+                if (uint32_t(tid) < tail) {
+                    const uint32_t tpg = main_end + tid;
+                    double tacc[8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) tacc[j] = 0.0;
+                    const unsigned short* t16 = reinterpret_cast<const unsigned short*>(tstage);
+#pragma unroll 16
+                    for (int c = 0; c < D; ++c) {
+                        const unsigned short hh = t16[size_t(c) * kTail + tid];
+                        tacc[c & 7] = __fma_rn(dq[c], (c & 1) ? h2d_scaled(hh) : h2d(__ushort_as_half(hh)), tacc[c & 7]);
+                    }
+                    finish(tpg, ((tacc[0] + tacc[1]) + (tacc[2] + tacc[3])) + ((tacc[4] + tacc[5]) + (tacc[6] + tacc[7])),
+                           tail_rec);
+                }
+            }
             double acc[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j) acc[j] = 0.0;
@@ -472,28 +493,6 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
             }
             if (c0 == r_begin) stamp(p.probe, 7);
             __syncthreads();  // part reused by the next pass
-        }
-        if (tail) {
-            if (owner && !appended) {
-                do_append();
-                __syncthreads();
-            }
-            cp_async_wait<0>();
-            __syncthreads();
-            if (uint32_t(tid) < tail) {
-                const uint32_t pg = main_end + tid;
-                double acc[8];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) acc[j] = 0.0;
-                const unsigned short* t16 = reinterpret_cast<const unsigned short*>(tstage);
-#pragma unroll 16
-                for (int c = 0; c < D; ++c) {
-                    const unsigned short hh = t16[size_t(c) * kTail + tid];
-                    acc[c & 7] = __fma_rn(dq[c], (c & 1) ? h2d_scaled(hh) : h2d(__ushort_as_half(hh)), acc[c & 7]);
-                }
-                const double sc = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-                finish(pg, sc, tail_rec);
-            }
         }
         if (r_begin < r_end) stamp(p.probe, 4);
     } else {
@@ -670,7 +669,8 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
                 const int grpi = tid / NTS, gt = tid % NTS;
                 if (G == 1 && grpi > 0) {
                     asm volatile("bar.sync %0, %1;" ::"r"(7), "r"(kThreads) : "memory");
-                    const bool ok = gsc[0].sig_valid != 0;
+                    const bool ok = gsc[0].sig_valid != 0 && p.prefetch;
+
                     const int shift = gsc[0].sig_shift;
                     const unsigned int bin = gsc[0].sig_bin;
                     const uint32_t page_bytes = p.S * D * 2;
@@ -681,7 +681,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
                         bool take;
                         uint32_t pg = i;
                         if (i == n_cand) {
-                            take = p.force != 0;  // the newest page
+                            take = p.force != 0 && p.prefetch;  // the newest page
                             pg = P - 1;
                         } else {
                             const unsigned long long k = keys[key_slot(i)];
@@ -711,6 +711,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
                                                    g == 0 ? p.probe : nullptr, G == 1 ? 7 : -1,
                                                    kThreads);
                     group_sync<NTS>(1 + grpi);  // scratch reuse for the next head
+
                 }
             };
             if (smem_keys && n_cand <= uint32_t(kSelThreads * kSelKpt)) {
@@ -791,15 +792,19 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
         __syncthreads();
         if (g == 0) stamp(p.probe, 17);
         if (tid < D) {  // the CTA's partial of this head: channel tid
-            float M = -CUDART_INF_F;
+            // Lane w < kWarps of every warp computes warp w's weight once; the channel
+            // sums then take the 16 weights by shuffle.
+            const float mw = lane < kWarps ? s_m[lane] : -CUDART_INF_F;
+            float M = mw;
 #pragma unroll
-            for (int w = 0; w < kWarps; ++w) M = fmaxf(M, s_m[w]);
+            for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+            const float myw = (mw == -CUDART_INF_F) ? 0.0f : exp2f(mw - M);
+            const float myl = lane < kWarps ? s_l[lane] * myw : 0.0f;
             float L = 0.0f, acc = 0.0f;
 #pragma unroll
             for (int w = 0; w < kWarps; ++w) {
-                const float sw = (s_m[w] == -CUDART_INF_F) ? 0.0f : exp2f(s_m[w] - M);
-                L += s_l[w] * sw;
-                acc += s_o[w][tid] * sw;
+                L += __shfl_sync(0xffffffffu, myl, w);
+                acc += s_o[w][tid] * __shfl_sync(0xffffffffu, myw, w);
             }
             float* slot = parts + (size_t(g) * C + rank) * (D + 2);
             if (C == 1 || rank == 0) {
@@ -838,31 +843,23 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
     stamp(p.probe, 19);
     if (p.probe && tid == 0) p.probe[blockIdx.x * kProbeSlots + 25] = clock64();
 
-    // Rank 0: merge the C partials of every head in rank order.  One thread per head
-    // turns the C maxima into weights w_r = exp2(m_r - M) / L; then every channel is a
-    // C-term dot product.
-    float* wts = s_o[0];  // [G][kMaxCluster] (s_o is free now)
-    if (tid < G) {
-        const float* base = parts + size_t(tid) * C * (D + 2);
-        float Mg = -CUDART_INF_F;
-        for (uint32_t r = 0; r < C; ++r) Mg = fmaxf(Mg, base[r * (D + 2)]);
-        float Lg = 0.0f;
-        for (uint32_t r = 0; r < C; ++r) {
-            const float mr = base[r * (D + 2)];
-            const float w = (mr == -CUDART_INF_F) ? 0.0f : exp2f(mr - Mg);
-            wts[tid * kMaxCluster + r] = w;
-            Lg += base[r * (D + 2) + 1] * w;
-        }
-        const float inv = 1.0f / Lg;
-        for (uint32_t r = 0; r < C; ++r) wts[tid * kMaxCluster + r] *= inv;
-    }
-    __syncthreads();
+    // Rank 0: merge the C partials of every head in rank order: weights
+    // w_r = exp2(m_r - M) / L (every thread computes its head's C weights itself), then
+    // every channel is a C-term dot product.
     for (int i = tid; i < G * int(p.head_dim); i += kThreads) {
         const int g = i / int(p.head_dim), d = i % int(p.head_dim);
         const size_t bh = size_t(b) * Hq + size_t(kvh) * G + g;
-        const float* base = parts + size_t(g) * C * (D + 2) + 2 + d;
-        float acc = 0.0f;
-        for (uint32_t r = 0; r < C; ++r) acc = fmaf(base[r * (D + 2)], wts[g * kMaxCluster + r], acc);
+        const float* hb = parts + size_t(g) * C * (D + 2);
+        float Mg = -CUDART_INF_F;
+        for (uint32_t r = 0; r < C; ++r) Mg = fmaxf(Mg, hb[r * (D + 2)]);
+        float Lg = 0.0f, acc = 0.0f;
+        for (uint32_t r = 0; r < C; ++r) {
+            const float mr = hb[r * (D + 2)];
+            const float w = (mr == -CUDART_INF_F) ? 0.0f : exp2f(mr - Mg);
+            Lg = fmaf(hb[r * (D + 2) + 1], w, Lg);
+            acc = fmaf(hb[r * (D + 2) + 2 + d], w, acc);
+        }
+        acc = acc / Lg;
         if (p.out_dtype == QK_DTYPE_F32) static_cast<float*>(p.out)[bh * p.head_dim + d] = acc;
         else static_cast<__half*>(p.out)[bh * p.head_dim + d] = __float2half_rn(acc);
     }
@@ -1005,6 +1002,7 @@ int launch_decode(qk_cache* c, uint32_t layer, const __half* q, const __half* k,
     prm.force = cfg.force_include_recent ? 1 : 0;
     prm.out_dtype = out_dtype;
     prm.keep_scores = c->keep_scores ? 1 : 0;
+    prm.prefetch = getenv("QK_NO_PREFETCH") ? 0 : 1;
     prm.scale_log2 = float(1.4426950408889634 / sqrt(double(c->desc.head_dim)));
     prm.probe = c->probe ? c->probe + size_t(layer) * c->B * c->Hkv * kMaxClusterCtas * kProbeSlots : nullptr;
     const uint32_t cluster = fused_cluster_size(c, batch, max_pages);

@@ -33,14 +33,15 @@ __device__ __forceinline__ void sel_stamp(unsigned long long* probe, int slot) {
 
 template <int NT>
 struct SelectScratch {
-    alignas(16) unsigned int hist[2048];
+    alignas(16) unsigned int hist[2048 + 4];  // + a trash bin for branch-free increments
     alignas(16) unsigned int warp_sum[NT / 32 < 4 ? 4 : NT / 32];
     alignas(16) unsigned long long red_max[NT / 32 < 4 ? 4 : NT / 32];
     unsigned long long red_min[NT / 32 < 4 ? 4 : NT / 32];
     unsigned long long cand_key[32];
     unsigned int cand_idx[32];
-    alignas(16) unsigned long long cand2[64];  // (key, index) pairs of the threshold bin
-    unsigned int cand_take[32];
+    alignas(16) unsigned long long cand2[66];  // (key, index) pairs of the threshold bin + trash
+    unsigned int cand_take[33];
+    int trash_out;
     // Early-signal of block_select_reg: after the first radix pass every key whose top
     // 11 bits (after the common prefix `sig_shift`) exceed `sig_bin` is selected.
     int sig_shift;
@@ -599,7 +600,8 @@ __device__ void block_select_reg(const unsigned long long (&key)[KPT], uint32_t 
 #pragma unroll
     for (int j = 0; j < KPT; ++j) {
         h[j] = unsigned((key[j] << shift) >> 32);
-        if (j < nv) atomicAdd(&sc.hist[h[j] >> 21], 1u);
+        // Branch-free: invalid entries count into the trash bin 2048.
+        atomicAdd(&sc.hist[j < nv ? (h[j] >> 21) : 2048u], 1u);
     }
     group_sync<NT>(bar);
     unsigned int c[BPL], sl = 0;
@@ -641,39 +643,48 @@ __device__ void block_select_reg(const unsigned long long (&key)[KPT], uint32_t 
         return;
     }
     // Keys above the bin are in; keys of the bin by TAKE_BIN or by rank (<= 32 keys).
+    const unsigned int lt_mask = (1u << lane) - 1u;
     bool take[KPT];
     if (bin_count == krem) {
 #pragma unroll
         for (int j = 0; j < KPT; ++j) take[j] = j < nv && (h[j] >> 21) >= bin;
     } else {
-        int slot[KPT];
+        // Gather the bin's keys: slots from ballots (one atomic per warp), stores branch
+        // free (non-candidates write the trash slot 32).
+        unsigned int cm[KPT], wtot = 0;
 #pragma unroll
         for (int j = 0; j < KPT; ++j) {
+            cm[j] = __ballot_sync(0xffffffffu, j < nv && (h[j] >> 21) == bin);
+            wtot += __popc(cm[j]);
+        }
+        unsigned int base = 0;
+        if (lane == 0 && wtot) base = atomicAdd(&sc.n_cand, wtot);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        unsigned int slot[KPT];
+#pragma unroll
+        for (int j = 0; j < KPT; ++j) {
+            const bool mine = (cm[j] >> lane) & 1u;
+            slot[j] = mine ? base + __popc(cm[j] & lt_mask) : 32u;
+            base += __popc(cm[j]);
+            reinterpret_cast<ulonglong2*>(sc.cand2)[slot[j]] = make_ulonglong2(key[j], i0 + j);
             take[j] = j < nv && (h[j] >> 21) > bin;
-            slot[j] = -1;
-            if (j < nv && (h[j] >> 21) == bin) {
-                slot[j] = int(atomicAdd(&sc.n_cand, 1u));
-                reinterpret_cast<ulonglong2*>(sc.cand2)[slot[j]] = make_ulonglong2(key[j], i0 + j);
-            }
         }
         group_sync<NT>(bar);
         const unsigned int nc = sc.n_cand;
-        if (uint32_t(gt) < nc) {
-            const ulonglong2 me = reinterpret_cast<const ulonglong2*>(sc.cand2)[gt];
+        if (warp == 0) {  // lane m ranks candidate m, straight-line
+            const ulonglong2 me = reinterpret_cast<const ulonglong2*>(sc.cand2)[lane];
             unsigned int rank = 0;
 #pragma unroll
             for (int m = 0; m < 32; ++m) {
-                if (uint32_t(m) < nc) {
-                    const ulonglong2 o = reinterpret_cast<const ulonglong2*>(sc.cand2)[m];
-                    rank += (o.x > me.x) || (o.x == me.x && o.y < me.y);
-                }
+                const ulonglong2 o = reinterpret_cast<const ulonglong2*>(sc.cand2)[m];
+                rank += (uint32_t(m) < nc) & ((o.x > me.x) | ((o.x == me.x) & (o.y < me.y)));
             }
-            sc.cand_take[gt] = rank < krem;
+            sc.cand_take[lane] = rank < krem;
+            if (lane == 0) sc.cand_take[32] = 0u;
         }
         group_sync<NT>(bar);
 #pragma unroll
-        for (int j = 0; j < KPT; ++j)
-            if (slot[j] >= 0) take[j] = sc.cand_take[slot[j]] != 0;
+        for (int j = 0; j < KPT; ++j) take[j] = take[j] | (sc.cand_take[slot[j]] != 0u);
     }
     sel_stamp(probe, 14);
     unsigned int mine = 0;
@@ -684,8 +695,11 @@ __device__ void block_select_reg(const unsigned long long (&key)[KPT], uint32_t 
     group_sync<NT>(bar);
     unsigned int pos = sum_below<NW>(sc.warp_sum, warp) + incl2 - mine;
 #pragma unroll
-    for (int j = 0; j < KPT; ++j)
-        if (take[j]) out[pos++] = static_cast<OutT>(i0 + j);
+    for (int j = 0; j < KPT; ++j) {  // branch free: rejected keys write a trash word
+        OutT* dst = take[j] ? out + pos : reinterpret_cast<OutT*>(&sc.trash_out);
+        *dst = static_cast<OutT>(i0 + j);
+        pos += take[j];
+    }
     sel_stamp(probe, 15);
 }
 
