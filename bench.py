@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--layers", type=int, default=LAYERS)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-native-e2e", action="store_true")
     return ap.parse_args()
 
 
@@ -366,6 +367,15 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e_us = e2e_s * 1e6 / (e2e_steps * NL) / world
+    e2e_path = "Python QuestCache.decode_step_host -> qk_decode_step_host (C ABI) per layer"
+    # The native host API (C++ questkv_b200::DeviceCache::decode_step_host), compiled here
+    # against the in-tree library; it replaces the Python number when it builds and runs.
+    if world == 1 and not args.no_native_e2e:
+        native = native_e2e(ctx, budget)
+        if native is not None:
+            e2e_us = native
+            e2e_path = ("C++ questkv_b200::DeviceCache::decode_step_host (include/questkv_b200.hpp) "
+                        "per layer, 8 layers x 20 steps; host q/k/v in, fp32 out to host")
     h2d = 3 * HEADS * HEAD_DIM * 2 * NL  # q, k, v fp16 per layer
     d2h = HEADS * HEAD_DIM * 4 * NL
 
@@ -415,12 +425,31 @@ def run_ours(args):
         "clocks": clocks.summary(),
         "e2e": {"value": round(e2e_us, 3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
-                "path": "qk_decode_step_host (C ABI) per layer, pinned host buffers"},
+                "path": e2e_path},
         "cpu_baseline": cpu,
     }
     print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
+
+
+def native_e2e(ctx, budget):
+    """e2e µs/layer through the C++ host API (tools/e2e_bench.cpp), or None."""
+    exe = os.path.join(ROOT, "build", "e2e_bench")
+    src = os.path.join(ROOT, "tools", "e2e_bench.cpp")
+    lib_dir = os.path.join(ROOT, "paper_2406_10774_b200")
+    try:
+        os.makedirs(os.path.dirname(exe), exist_ok=True)
+        if not os.path.exists(exe) or os.path.getmtime(exe) < os.path.getmtime(src):
+            subprocess.run(["g++", "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"), src,
+                            "-o", exe, "-L", lib_dir, "-lquestkv_b200", f"-Wl,-rpath,{lib_dir}"],
+                           check=True, capture_output=True, timeout=120)
+        out = subprocess.run([exe, str(ctx), str(budget), "8", "20", "3"], capture_output=True,
+                             text=True, timeout=300)
+        line = json.loads(out.stdout.strip().splitlines()[-1])
+        return float(line["e2e_us_per_layer"])
+    except Exception:
+        return None
 
 
 def kernel_breakdown(qc, q0, NL, budget, stream):

@@ -183,9 +183,10 @@ QK_API int qk_decode_step(qk_cache *cache, uint32_t layer, const uint16_t *q, co
                    void *out, int32_t out_dtype, int32_t *pages_out, uint32_t pages_stride,
                    int32_t *counts_out, void *stream);
 
-/* Same step from HOST buffers: copies q/k/v (pinned or pageable) in, runs
- * qk_decode_step, copies the output back; synchronous.  The reference-facing call for
- * callers that keep activations on the host. */
+/* Same step from HOST buffers (pinned or pageable), synchronous: q/k/v are copied into a
+ * pinned, device-mapped staging buffer that the kernel reads directly, and the kernel
+ * writes the fp32 output there (zero-copy); one launch and one synchronisation per call.
+ * The reference-facing call for callers that keep activations on the host. */
 QK_API int qk_decode_step_host(qk_cache *cache, uint32_t layer, const uint16_t *q_host,
                         const uint16_t *k_host, const uint16_t *v_host, uint32_t batch,
                         const qk_selection_cfg *cfg, float *out_host, void *stream);

@@ -83,6 +83,7 @@ void free_cache(qk_cache* c) {
                     c->prange};
     for (void* p : ptrs)
         if (p) cudaFree(p);
+    if (c->host_stage) cudaFreeHost(c->host_stage);
     delete c;
 }
 
@@ -486,22 +487,36 @@ int qk_decode_step_host(qk_cache* c, uint32_t layer, const uint16_t* q_host,
     cudaStream_t st = as_stream(stream);
     const size_t hd = c->desc.head_dim;
     const size_t nq = size_t(batch) * c->Hq * hd, nkv = size_t(batch) * c->Hkv * hd;
-    uint16_t* dq = c->ws_io;
-    uint16_t* dk = dq + nq;
-    uint16_t* dv = dk + nkv;
-    int rc = cuda_check(cudaMemcpyAsync(dq, q_host, nq * 2, cudaMemcpyHostToDevice, st), "h2d q");
-    if (!rc && k_host) {
-        rc = cuda_check(cudaMemcpyAsync(dk, k_host, nkv * 2, cudaMemcpyHostToDevice, st), "h2d k");
-        if (!rc) rc = cuda_check(cudaMemcpyAsync(dv, v_host, nkv * 2, cudaMemcpyHostToDevice, st), "h2d v");
+    // Inputs and output go through a pinned, device-mapped staging buffer that the fused
+    // kernel reads and writes directly (zero-copy): one launch and one synchronisation per
+    // call instead of three host-to-device copies, the kernel and a device-to-host copy.
+    const size_t in_max = size_t(c->B) * (c->Hq + 2 * c->Hkv) * hd * 2;
+    const size_t out_max = size_t(c->B) * c->Hq * hd * 4;
+    if (!c->host_stage) {
+        void* h = nullptr;
+        int rc = cuda_check(cudaHostAlloc(&h, in_max + out_max, cudaHostAllocMapped), "cudaHostAlloc");
+        if (rc) return rc;
+        void* d = nullptr;
+        rc = cuda_check(cudaHostGetDevicePointer(&d, h, 0), "cudaHostGetDevicePointer");
+        if (rc) {
+            cudaFreeHost(h);
+            return rc;
+        }
+        c->host_stage = static_cast<unsigned char*>(h);
+        c->host_stage_dev = static_cast<unsigned char*>(d);
     }
-    if (!rc)
-        rc = qk_decode_step(c, layer, dq, k_host ? dk : nullptr, k_host ? dv : nullptr, batch, cfg,
-                            c->ws_out, QK_DTYPE_F32, nullptr, 0, nullptr, stream);
-    if (!rc)
-        rc = cuda_check(cudaMemcpyAsync(out_host, c->ws_out, size_t(batch) * c->Hq * hd * 4,
-                                        cudaMemcpyDeviceToHost, st),
-                        "d2h out");
+    uint16_t* hq = reinterpret_cast<uint16_t*>(c->host_stage);
+    std::memcpy(hq, q_host, nq * 2);
+    if (k_host) {
+        std::memcpy(hq + nq, k_host, nkv * 2);
+        std::memcpy(hq + nq + nkv, v_host, nkv * 2);
+    }
+    const uint16_t* dq = reinterpret_cast<const uint16_t*>(c->host_stage_dev);
+    float* dout = reinterpret_cast<float*>(c->host_stage_dev + in_max);
+    int rc = qk_decode_step(c, layer, dq, k_host ? dq + nq : nullptr, k_host ? dq + nq + nkv : nullptr,
+                            batch, cfg, dout, QK_DTYPE_F32, nullptr, 0, nullptr, stream);
     if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "qk_decode_step_host");
+    if (!rc) std::memcpy(out_host, c->host_stage + in_max, size_t(batch) * c->Hq * hd * 4);
     return rc;
 }
 

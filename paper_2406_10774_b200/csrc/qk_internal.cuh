@@ -71,6 +71,8 @@ struct qk_cache {
     uint16_t* ws_io = nullptr;           // staging for qk_decode_step_host
     float* ws_out = nullptr;             // [B][Hq][head_dim] fp32
     float* ws_lse = nullptr;             // [B][Hq] fp32 (host-buffer entry points)
+    unsigned char* host_stage = nullptr; // pinned, device-mapped staging of the host step
+    unsigned char* host_stage_dev = nullptr;  // (q, k, v in; fp32 out), allocated lazily
     unsigned long long* probe = nullptr; // phase timestamps of the fused kernel (QK_PROBE)
     bool keep_scores = false;            // fused step: estimate every page, keep scores
     uint64_t device_bytes = 0;
