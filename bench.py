@@ -42,15 +42,31 @@ UNIT = "us/layer"
 HEADS, HEAD_DIM, PAGE, CTX, BUDGET, LAYERS = 32, 128, 16, 32768, 2048, 32
 
 
+CONFIGS = {
+    # name: (q heads, kv heads, context, budget, batch, layers, description)
+    "cfg1": (32, 32, 8192, 1024, 1, 32, "cfg1: Llama-2-7B attention (32 heads MHA, d=128, page 16), "
+             "8K context, budget 1024, batch 1"),
+    "cfg2": (32, 32, 32768, 2048, 1, 32, "cfg2: Llama-2-7B attention shape (32 heads MHA, d=128, "
+             "page 16), 32K context, token budget 2048, batch 1 per GPU"),
+    "cfg3": (32, 32, 131072, 4096, 1, 8, "cfg3: LongChat-7B attention (32 heads MHA, d=128, page 16), "
+             "128K context, budget 4096, batch 1 per GPU"),
+    "cfg4": (32, 8, 65536, 2048, 32, 2, "cfg4: Llama-3-8B GQA attention (32 q / 8 kv heads, d=128, "
+             "page 16), 64K context, budget 2048, batch 32 per GPU"),
+    "cfg5": (32, 32, 32768, 2048, 8, 32, "cfg5: Llama-2-7B decode loop, 32 layers x (append + "
+             "estimate + top-K + attend), 32K context, budget 2048, batch 8 per GPU"),
+}
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--ctx", type=int, default=CTX)
-    ap.add_argument("--budget", type=int, default=BUDGET)
-    ap.add_argument("--layers", type=int, default=LAYERS)
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="cfg2")
+    ap.add_argument("--ctx", type=int, default=None)
+    ap.add_argument("--budget", type=int, default=None)
+    ap.add_argument("--layers", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-native-e2e", action="store_true")
@@ -210,16 +226,19 @@ def run_reference(args):
     if not os.path.exists(REF_SO):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return
+    HQ, _, ctx0, budget0, _, _, desc = CONFIGS[args.config]
+    ctx = args.ctx if args.ctx else ctx0
+    budget = args.budget if args.budget else budget0
     rng = np.random.default_rng(1)
     sd = 1.0 / np.sqrt(HEAD_DIM)
-    keys = (rng.standard_normal((HEADS, args.ctx, HEAD_DIM), dtype=np.float32) * sd)
+    keys = (rng.standard_normal((HEADS, ctx, HEAD_DIM), dtype=np.float32) * sd)
     keys = keys.astype(np.float16).astype(np.float32)
-    vals = (rng.standard_normal((HEADS, args.ctx, HEAD_DIM), dtype=np.float32) * sd)
+    vals = (rng.standard_normal((HEADS, ctx, HEAD_DIM), dtype=np.float32) * sd)
     vals = vals.astype(np.float16).astype(np.float32)
     q = (rng.standard_normal((HEADS, HEAD_DIM)) * sd).astype(np.float16).astype(np.float32)
     layer = Reference().layer(keys, vals, PAGE)
     steps = max(1, min(args.steps, 20))
-    mean_ns, min_ns, _ = layer.step(q, args.budget, threads=threads, warmup=max(1, min(args.warmup, 3)),
+    mean_ns, min_ns, _ = layer.step(q, budget, threads=threads, warmup=max(1, min(args.warmup, 3)),
                                     reps=steps)
     layer.close()
     us = mean_ns / 1e3
@@ -228,17 +247,20 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": steps, "warmup": max(1, min(args.warmup, 3)),
         "ms_per_step": round(mean_ns / 1e6, 4), "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic N(0,1/d) fp16-representable",
-        "config": {"workload": "cfg2: Llama-2-7B attention (32 heads, d=128, S=16), 32K ctx, "
-                               "budget 2048, batch 1; one layer per step on the host CPU",
-                   "seq_len": args.ctx, "budget": args.budget, "heads": HEADS},
+        "config": {"workload": desc + "; one layer (one sequence, 32 heads) per step on the host "
+                               "CPU",
+                   "name": args.config,
+                   "seq_len": ctx, "budget": budget, "heads": HEADS},
         "cpu_baseline": {"value": round(us, 3), "unit": UNIT, "cores": threads,
                          "kind": "reference",
-                         "sample": f"every step = 1 full layer ({HEADS} heads x {args.ctx} tokens)"},
+                         "sample": f"every step = 1 full layer ({HEADS} heads x {ctx} tokens)"},
         "e2e": {"value": round(us, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "min_us_per_layer": round(min_ns / 1e3, 3),
     }
     print(json.dumps(line))
+
+
 
 
 def run_ours(args):
@@ -253,34 +275,39 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    NL, ctx, budget = args.layers, args.ctx, args.budget
+    HQ, HKV, ctx0, budget0, B, NL0, desc = CONFIGS[args.config]
+    ctx = args.ctx if args.ctx else ctx0
+    budget = args.budget if args.budget else budget0
+    NL = args.layers if args.layers else NL0
     headroom = args.warmup + args.steps + args.e2e_steps + 8
-    qc = QuestCache(HEAD_DIM, PAGE, num_layers=NL, max_batch=1, num_q_heads=HEADS,
-                    max_tokens=ctx + headroom, device=local)
+    qc = QuestCache(HEAD_DIM, PAGE, num_layers=NL, max_batch=B, num_q_heads=HQ,
+                    num_kv_heads=HKV, max_tokens=ctx + headroom, device=local)
     g = torch.Generator(device=dev)
     g.manual_seed(1234 + rank)
     sd = 1.0 / HEAD_DIM ** 0.5
-    n0 = ctx - 1  # the first timed step appends token ctx-1 -> a 32K context
+    n0 = ctx - 1  # the first timed step appends token ctx-1 -> a full `ctx` context
     for layer in range(NL):
-        k = (torch.randn((HEADS, n0, HEAD_DIM), generator=g, device=dev) * sd).half()
-        v = (torch.randn((HEADS, n0, HEAD_DIM), generator=g, device=dev) * sd).half()
-        qc.prefill(layer, 0, k, v)
-        del k, v
+        for bb in range(B):
+            k = (torch.randn((HKV, n0, HEAD_DIM), generator=g, device=dev) * sd).half()
+            v = (torch.randn((HKV, n0, HEAD_DIM), generator=g, device=dev) * sd).half()
+            qc.prefill(layer, bb, k, v)
+            del k, v
     total_steps = args.warmup + args.steps
-    q = (torch.randn((total_steps, NL, 1, HEADS, HEAD_DIM), generator=g, device=dev) * sd).half()
-    kn = (torch.randn((total_steps, NL, 1, HEADS, HEAD_DIM), generator=g, device=dev) * sd).half()
-    vn = (torch.randn((total_steps, NL, 1, HEADS, HEAD_DIM), generator=g, device=dev) * sd).half()
+    q = (torch.randn((total_steps, NL, B, HQ, HEAD_DIM), generator=g, device=dev) * sd).half()
+    kn = (torch.randn((total_steps, NL, B, HKV, HEAD_DIM), generator=g, device=dev) * sd).half()
+    vn = (torch.randn((total_steps, NL, B, HKV, HEAD_DIM), generator=g, device=dev) * sd).half()
     qbuf, kbuf, vbuf = q[0].clone(), kn[0].clone(), vn[0].clone()
-    out = torch.empty((NL, 1, HEADS, HEAD_DIM), dtype=torch.float32, device=dev)
+    out = torch.empty((NL, B, HQ, HEAD_DIM), dtype=torch.float32, device=dev)
     torch.cuda.synchronize()
 
     stream = torch.cuda.Stream(device=dev)
     # Load every kernel of the step eagerly on a throwaway cache of the same geometry
     # (lazy module loading must not happen inside the capture).
-    warm = QuestCache(HEAD_DIM, PAGE, num_layers=1, max_batch=1, num_q_heads=HEADS,
-                      max_tokens=ctx + headroom, device=local)
-    warm.prefill(0, 0, kn[0, 0].view(HEADS, 1, HEAD_DIM).contiguous(),
-                 vn[0, 0].view(HEADS, 1, HEAD_DIM).contiguous())
+    warm = QuestCache(HEAD_DIM, PAGE, num_layers=1, max_batch=B, num_q_heads=HQ,
+                      num_kv_heads=HKV, max_tokens=ctx + headroom, device=local)
+    for bb in range(B):
+        warm.prefill(0, bb, kn[0, 0, bb].view(HKV, 1, HEAD_DIM).contiguous(),
+                     vn[0, 0, bb].view(HKV, 1, HEAD_DIM).contiguous())
     warm.decode_step(0, qbuf[0], kbuf[0], vbuf[0], budget, stream=stream)
     stream.synchronize()
     warm.close()
@@ -291,8 +318,6 @@ def run_ours(args):
             qc.decode_step(layer, qbuf[layer], kbuf[layer], vbuf[layer], budget, out=out[layer],
                            stream=stream)
     kernels_per_step = qc.kernel_launches - launches0
-    # Host shadow lengths advanced once during capture; every replay advances the device
-    # lengths by one token per layer.
 
     def step(i):
         qbuf.copy_(q[i], non_blocking=True)
@@ -330,27 +355,28 @@ def run_ours(args):
     us_per_layer = ms_per_step * 1e3 / NL
     value = us_per_layer / world
 
-    # Algorithmic bytes of the timed steps (lengths ctx-1+warmup+1 .. ).
+    # Algorithmic bytes of the timed steps (reference accounting per query head, every
+    # sequence of the batch).
     bytes_total = 0
     for i in range(args.warmup, total_steps):
         L = ctx + i  # tokens after this step's append (first replay -> ctx)
-        bytes_total += algorithmic_bytes([L], HEADS, HEAD_DIM, PAGE, budget)
+        bytes_total += B * algorithmic_bytes([L], HQ, HEAD_DIM, PAGE, budget)
     bytes_per_layer = bytes_total / args.steps
     achieved_gbs = bytes_per_layer / (us_per_layer * 1e-6) / 1e9
     peak, peak_src = measured_peaks()
 
     # Per-kernel breakdown (one layer, eager, CUDA events) on the current state.
-    breakdown = kernel_breakdown(qc, q[0], NL, budget, stream) if rank == 0 else {}
+    breakdown = kernel_breakdown(qc, q[0], NL, budget, stream) if rank == 0 and B == 1 else {}
 
-    # End to end through the public C ABI with host buffers (qk_decode_step_host):
-    # H2D of q/k/v from pinned memory and D2H of the fp32 output inside the timed region.
-    qh = torch.empty((NL, 1, HEADS, HEAD_DIM), dtype=torch.float16).pin_memory()
-    kh = torch.empty_like(qh).pin_memory()
-    vh = torch.empty_like(qh).pin_memory()
+    # End to end with host buffers: H2D of q/k/v and D2H of the fp32 output inside the
+    # timed region (qk_decode_step_host: the kernel reads/writes pinned mapped staging).
+    qh = torch.empty((NL, B, HQ, HEAD_DIM), dtype=torch.float16).pin_memory()
+    kh = torch.empty((NL, B, HKV, HEAD_DIM), dtype=torch.float16).pin_memory()
+    vh = torch.empty_like(kh).pin_memory()
     qh.copy_(q[0].cpu())
     kh.copy_(kn[0].cpu())
     vh.copy_(vn[0].cpu())
-    oh = torch.empty((NL, 1, HEADS, HEAD_DIM), dtype=torch.float32).pin_memory()
+    oh = torch.empty((NL, B, HQ, HEAD_DIM), dtype=torch.float32).pin_memory()
     qn, kn_, vn_, on = qh.numpy(), kh.numpy(), vh.numpy(), oh.numpy()
     e2e_steps = max(1, args.e2e_steps)
     qc.decode_step_host(0, qn[0], kn_[0], vn_[0], budget, out=on[0], stream=stream)  # warm
@@ -370,21 +396,21 @@ def run_ours(args):
     e2e_path = "Python QuestCache.decode_step_host -> qk_decode_step_host (C ABI) per layer"
     # The native host API (C++ questkv_b200::DeviceCache::decode_step_host), compiled here
     # against the in-tree library; it replaces the Python number when it builds and runs.
-    if world == 1 and not args.no_native_e2e:
+    if world == 1 and not args.no_native_e2e and args.config == "cfg2":
         native = native_e2e(ctx, budget)
         if native is not None:
             e2e_us = native
             e2e_path = ("C++ questkv_b200::DeviceCache::decode_step_host (include/questkv_b200.hpp) "
                         "per layer, 8 layers x 20 steps; host q/k/v in, fp32 out to host")
-    h2d = 3 * HEADS * HEAD_DIM * 2 * NL  # q, k, v fp16 per layer
-    d2h = HEADS * HEAD_DIM * 4 * NL
+    h2d = (HQ + 2 * HKV) * B * HEAD_DIM * 2 * NL  # q, k, v fp16 per layer
+    d2h = HQ * B * HEAD_DIM * 4 * NL
 
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
     cpu = None
-    if not args.no_cpu_baseline and world == 1:
+    if not args.no_cpu_baseline and world == 1 and args.config == "cfg2":
         cpu = cpu_baseline_sample(ctx, budget, os.cpu_count() or 1)
     line = {
         "metric": METRIC,
@@ -400,32 +426,33 @@ def run_ours(args):
         "dtype": "fp16 storage, fp64 estimate, fp32 attention accumulate",
         "data": "synthetic N(0,1/d) fp16 K/V/q (random-init, generated on device)",
         "config": {
-            "workload": "cfg2: Llama-2-7B attention shape (32 heads MHA, d=128, page 16), "
-                        "32K context, token budget 2048, batch 1 per GPU; step = append+estimate"
-                        "+top-K+sparse attend over 32 distinct layer caches (CUDA graph)",
-            "seq_len": ctx, "budget": budget, "heads": HEADS, "head_dim": HEAD_DIM,
-            "page_size": PAGE, "layers_per_step": NL, "global_batch": world,
+            "workload": desc + "; step = append+estimate+top-K+sparse attend over "
+                        f"{NL} distinct layer caches (CUDA graph)",
+            "name": args.config, "seq_len": ctx, "budget": budget, "q_heads": HQ,
+            "kv_heads": HKV, "head_dim": HEAD_DIM, "page_size": PAGE, "layers_per_step": NL,
+            "batch_per_gpu": B, "global_batch": B * world,
             "parallelism": f"request-sharded x{world} (no collective)",
-            "l2": "inputs larger than L2: 32 rotating layer caches (17 GB), 67 MB touched per "
-                  "layer, each revisited after ~2 GB of other layers",
+            "l2": f"inputs larger than L2: {NL} rotating layer caches, each revisited after "
+                  f"{NL - 1} other layers' traffic",
         },
         "latency_us_per_layer": round(us_per_layer, 3),
+        "tokens_per_s": round(B * world * 1e6 / (us_per_layer * NL), 1),
         "achieved_hbm_gbs": round(achieved_gbs, 1),
         "roofline": {
             "bound": "hbm", "achieved": round(achieved_gbs, 1), "peak": peak, "unit": "GB/s",
-            "frac": round(achieved_gbs / peak, 4), "traffic": profiled_traffic(),
-            "kernel": "decode step (append+estimate+top-K+attend launches of one layer)",
+            "frac": round(achieved_gbs / peak, 4),
+            "traffic": profiled_traffic() if args.config == "cfg2" else None,
+            "kernel": "decode_fused_kernel (one launch = append+estimate+top-K+attend of a layer)",
             "bytes_per_launch": int(bytes_per_layer),
-            "bytes_model": "reference accounting metrics.cpp:105-106: 2*d*2B per page "
-                           "(metadata) + 2*d*2B per attended token",
+            "bytes_model": "reference accounting metrics.cpp:105-106: 2*d*2B per page (metadata) "
+                           "+ 2*d*2B per attended token, per query head",
             "peak_source": peak_src,
         },
         "kernel_breakdown_us": breakdown,
         "gpu_launches": int(kernels_per_step * args.steps),
         "clocks": clocks.summary(),
         "e2e": {"value": round(e2e_us, 3), "unit": UNIT, "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h,
-                "path": e2e_path},
+                "d2h_bytes_per_step": d2h, "path": e2e_path},
         "cpu_baseline": cpu,
     }
     print(json.dumps(line))
