@@ -13,6 +13,8 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libquestkv_b200.so")
+# Kernel A/B experiments point QK_LIB at another in-tree build (tools/ab_bench.sh).
+LIB_PATH = os.environ.get("QK_LIB", LIB_PATH)
 
 QK_OK = 0
 QK_ERR_INVALID_ARGUMENT = 1

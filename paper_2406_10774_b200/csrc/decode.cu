@@ -97,6 +97,19 @@ __device__ __forceinline__ void st_cluster_u64(uint32_t cluster_addr, unsigned l
     asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(cluster_addr), "l"(v) : "memory");
 }
 
+// Asynchronous remote shared-memory stores that complete transaction bytes on the
+// receiver's mbarrier (the receiver's wait is the only synchronisation they need).
+__device__ __forceinline__ void st_async_u64(uint32_t cluster_addr, unsigned long long v, uint32_t cluster_bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(cluster_addr),
+                 "l"(v), "r"(cluster_bar)
+                 : "memory");
+}
+__device__ __forceinline__ void st_async_f32(uint32_t cluster_addr, float v, uint32_t cluster_bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f32 [%0], %1, [%2];" ::"r"(cluster_addr),
+                 "f"(v), "r"(cluster_bar)
+                 : "memory");
+}
+
 // mbarrier + bulk-copy (TMA 1D) helpers.
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
@@ -104,6 +117,13 @@ __device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t coun
 __device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                  "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx_only(unsigned long long* bar, uint32_t bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cluster.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote_release(uint32_t cluster_bar) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
     asm volatile(
@@ -208,9 +228,18 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
     __shared__ float s_o[kWarps][D];
     __shared__ float s_m[kWarps], s_l[kWarps];
 
-    __shared__ __align__(8) unsigned long long merge_bar[1];  // rank 0: peers' partials
+    // merge_bar (rank 0): the peers' partials land on it (st.async, transaction bytes).
+    // keys_bar (every CTA): every CTA of the cluster arrives once with release after its
+    // estimate (its scores, the appended K/V row and its read of the old length are then
+    // visible), and the pushed selection keys complete transaction bytes on it.
+    __shared__ __align__(8) unsigned long long merge_bar[1], keys_bar[1];
     if (threadIdx.x == 0) {
-        mbar_init(merge_bar, C - 1 > 0 ? C - 1 : 1);
+        mbar_init(merge_bar, 1);
+        mbar_init(keys_bar, C);
+        if (C > 1 && cluster_rank() == 0)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(merge_bar)),
+                         "r"(uint32_t((C - 1) * G * (D + 2) * 4))
+                         : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     const uint32_t unit = blockIdx.x / C;
@@ -297,6 +326,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
     const uint32_t n_cand = all_pages ? 0u : (p.force ? P - 1 : P);
     const uint32_t n_est = p.keep_scores ? P : n_cand;
     const bool smem_keys = p.key_cap != 0 && key_slots(n_cand) <= p.key_cap;
+    if (tid == 0 && smem_keys && n_cand > 0) mbar_expect_tx_only(keys_bar, uint32_t(G) * n_cand * 8u);
     // This CTA's estimate range: contiguous, a multiple of 8 pages (16-byte metadata
     // pieces), balanced over the cluster.
     const uint32_t per = ((n_est + C - 1) / C + 7) & ~7u;
@@ -311,7 +341,19 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
     const bool patch = owner && new_page < n_est;  // staged copy to patch
     __shared__ __half s_new_min[D], s_new_max[D];
     __shared__ uint32_t s_rec_scratch[D / 32];
-    bool appended = false;
+    bool appended = false, arrived = false;
+    // Each CTA arrives once on every CTA's keys_bar; with release when it wrote data its
+    // peers read (the owner's new K/V row, scores through HBM).
+    auto arrive_keys = [&](bool release) {
+        if (tid == 0) {
+            if (release) asm volatile("fence.acq_rel.cluster;" ::: "memory");
+            for (uint32_t r = 0; r < C; ++r)
+                asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                                 map_rank(keys_bar, r))
+                             : "memory");
+        }
+        arrived = true;
+    };
     auto do_append = [&]() {
         if (tid < D) {
             const uint32_t c = tid, row = t_old % p.S;
@@ -419,12 +461,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
             if (smem_keys) {
                 if (pg < n_cand) {
                     const unsigned long long k = order_key(sc);
-                    const uint32_t a = smem_u32(keys + key_slot(pg));
-                    for (uint32_t r = 0; r < C; ++r) {
-                        uint32_t ra;
-                        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(r));
-                        st_cluster_u64(ra, k);
-                    }
+                    for (uint32_t r = 0; r < C; ++r) st_async_u64(map_rank(keys + key_slot(pg), r), k, map_rank(keys_bar, r));
                 }
             }
             if (!smem_keys || p.keep_scores)
@@ -444,8 +481,11 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
                 v[k] = act ? ld_nc_v4(mslice + (size_t(minmax) * D + c) * p.mrow + pbase)
                            : make_int4(0, 0, 0, 0);
             }
-            if (owner && !appended) do_append();  // overlaps the loads above; s_new_* are
-                                                  // read after the barrier below
+            // The append overlaps the loads above (s_new_* are read after the barrier below).
+            if (owner && !appended) {
+                do_append();
+                if (smem_keys) arrive_keys(true);  // the new K/V row released early
+            }
             if (tail && c0 == r_begin) {
                 // The staged tail pages (issued first) are finished while this pass's
                 // register loads are still in flight.
@@ -622,12 +662,8 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
                         if (pg < n_cand) {
                             // Push the key to every CTA of the cluster (padded slot).
                             const unsigned long long k = order_key(sc);
-                            const uint32_t a = smem_u32(keys + size_t(g) * p.key_cap + key_slot(pg));
-                            for (uint32_t r = 0; r < C; ++r) {
-                                uint32_t ra;
-                                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(r));
-                                st_cluster_u64(ra, k);
-                            }
+                            unsigned long long* dst = keys + size_t(g) * p.key_cap + key_slot(pg);
+                            for (uint32_t r = 0; r < C; ++r) st_async_u64(map_rank(dst, r), k, map_rank(keys_bar, r));
                         }
                     }
                     if (!smem_keys || p.keep_scores)
@@ -643,9 +679,10 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
     // Keys of every CTA of the unit are visible after this barrier (and so is the new K/V
     // row written in phase A).
     stamp(p.probe, 8);
-    cluster_sync_acqrel();
+    if (!arrived) arrive_keys(!smem_keys || owner);
+    mbar_wait_cluster(keys_bar, 0);
     stamp(p.probe, 9);
-    if (append && rank == 0 && tid == 0) {
+    if (append && rank == 0 && tid == kThreads - 1) {  // off the selection warps' path
         // Every CTA of this unit has read the old length.  The last unit of the sequence
         // to get here publishes the new length for the next step.
         if (atomicAdd(p.len_ticket + p.layer * p.B + b, 1) == int(p.Hkv) - 1) {
@@ -814,10 +851,11 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
                     slot[1] = L;
                 }
             } else {
-                st_cluster_f32(slot + 2 + tid, 0, acc);
+                const uint32_t rb = map_rank(merge_bar, 0);
+                st_async_f32(map_rank(slot + 2 + tid, 0), acc, rb);
                 if (tid == 0) {
-                    st_cluster_f32(slot, 0, M);
-                    st_cluster_f32(slot + 1, 0, L);
+                    st_async_f32(map_rank(slot, 0), M, rb);
+                    st_async_f32(map_rank(slot + 1, 0), L, rb);
                 }
             }
         }
@@ -825,17 +863,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
     }
     asm volatile("griddepcontrol.launch_dependents;");
     stamp(p.probe, 18);
-    if (C > 1 && rank != 0) {
-        // Signal rank 0 (release: the partial stores above are ordered before it), then
-        // exit: no CTA reads this CTA's shared memory any more.
-        if (tid == 0) {
-            asm volatile("fence.acq_rel.cluster;" ::: "memory");
-            asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
-                             map_rank(merge_bar, 0))
-                         : "memory");
-        }
-        return;
-    }
+    if (C > 1 && rank != 0) return;  // the partials complete on rank 0's merge_bar
     if (C > 1) {
         if (tid == 0) mbar_wait_cluster(merge_bar, 0);  // every peer's partial has landed
         __syncthreads();
