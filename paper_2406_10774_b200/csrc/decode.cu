@@ -283,6 +283,26 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
     // split-estimate certificate, phase B).
     __shared__ double s_qabs[G];
     __shared__ unsigned int s_qcode[G];
+    __shared__ double s_qpart[D / 32];
+    __shared__ unsigned int s_qcodep[D / 32];
+    if constexpr (G == 1) {
+        // Thread c < D holds channel c: its weight, its row and its warp's share of the
+        // q statistics (per-warp partials: sum|q| of fp16 values is exact in any order).
+        if (tid < D) {
+            const double x = double(__half2float(qv[0]));
+            dq[tid] = (tid & 1) ? x * 0x1p1008 : x;
+            need[tid] = (x < 0.0) ? 2 : 1;
+            double a = fabs(x);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);  // exact
+            const unsigned int code = __reduce_min_sync(0xffffffffu, ulp_code(__half_as_ushort(qv[0])));
+            if (lane == 0) {
+                s_qpart[warp] = a;
+                s_qcodep[warp] = code;
+            }
+        }
+        __syncthreads();
+    } else {
     if (tid < G) {
         s_qabs[tid] = 0.0;
         s_qcode[tid] = 31u;
@@ -317,6 +337,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
         need[c] = m;
     }
     __syncthreads();
+    }
     stamp(p.probe, 2);
 
     // Selection shape (criticality.cpp:47-59): K >= P -> every page; with force-recent
@@ -436,11 +457,18 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
 
         // The certificate, the sequential fallback and the hand-off of one page's score.
         auto finish = [&](uint32_t pg, double sc, uint32_t rec) {
-            const uint32_t xcode = rec >> 16, qcode = s_qcode[0];
+            double qabs = 0.0;
+            unsigned int qcode = 31u;
+#pragma unroll
+            for (int w = 0; w < D / 32; ++w) {
+                qabs += s_qpart[w];
+                qcode = min(qcode, s_qcodep[w]);
+            }
+            const uint32_t xcode = rec >> 16;
             bool exact = xcode >= 31u || qcode >= 31u;
             if (!exact) {
                 const double bound = __dmul_ru(
-                    s_qabs[0], double(__half2float(__ushort_as_half(uint16_t(rec & 0x7fffu)))));
+                    qabs, double(__half2float(__ushort_as_half(uint16_t(rec & 0x7fffu)))));
                 const int e = 5 + int(qcode) + int(xcode);
                 exact = bound < __longlong_as_double(static_cast<long long>(e + 1023) << 52);
             }
@@ -826,9 +854,11 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
             s_m[warp] = m;
             s_l[warp] = l;
         }
+        __syncwarp();  // reconverge the half-warp stores before the aligned barrier
         __syncthreads();
         if (g == 0) stamp(p.probe, 17);
         if (tid < D) {  // the CTA's partial of this head: channel tid
+            __syncwarp();  // converged shuffles below (no divergent fallback path)
             // Lane w < kWarps of every warp computes warp w's weight once; the channel
             // sums then take the 16 weights by shuffle.
             const float mw = lane < kWarps ? s_m[lane] : -CUDART_INF_F;

@@ -46,7 +46,7 @@ buf = np.zeros(n * args.layers, dtype=np.uint64)
 lib = _lib.load()
 names = {0: "entry", 1: "dep_wait", 2: "prologue", 21: "pre_cwait", 22: "cluster_wait", 3: "loads_issued", 5: "w0_computed", 6: "partials_synced", 7: "pushed", 4: "est_loop_end", 8: "estimate_end", 9: "barrier1", 10: "keys_pulled",
          11: "sel_pass0", 26: "pair_gathered", 27: "pair_sync1", 28: "pair_ranked", 29: "pair_sync2", 12: "sel_pass1", 13: "sel_pass2", 14: "sel_pair", 15: "sel_compact",
-         29: "idle_fold_end", 30: "sel_fold_end", 16: "select_end", 31: "combined", 17: "attend_end", 18: "partials", 19: "barrier2", 20: "merged"}
+         29: "x29", 30: "x30", 16: "select_end", 31: "x31", 17: "attend_end", 18: "partials", 19: "barrier2", 20: "merged"}
 for _ in range(50):  # clocks up
     for layer in range(args.layers):
         qc.decode_step(layer, q, None, None, args.budget, out=out)
