@@ -39,7 +39,10 @@ constexpr int kSelGroups = kThreads / kSelThreads;
 constexpr int kSelKpt = 16;             // keys per thread of a selection group
 constexpr uint32_t kMaxFusedK = 512;    // selected pages per query head kept in smem
 constexpr uint32_t kMaxCluster = 16;
-constexpr size_t kKeysBudget = 40 * 1024;  // cluster-exchanged selection keys per CTA
+// Cluster-exchanged selection keys per CTA (MHA has no metadata stage in shared memory,
+// so its budget covers 128K-token contexts).
+constexpr size_t keys_budget(int G) { return G == 1 ? 96 * 1024 : 40 * 1024; }
+constexpr uint32_t kTail = 64;  // MHA: pages past the 512-page passes staged with cp.async
 constexpr size_t kMaxSmem = 227 * 1024 - 8 * 1024;  // opt-in limit minus static smem
 
 __device__ __forceinline__ double h2d(__half h) {
@@ -60,10 +63,13 @@ __device__ __forceinline__ double h2d_scaled(unsigned short h) {
 }
 
 __device__ __forceinline__ void stamp(unsigned long long* probe, int slot) {
-    if (probe != nullptr && threadIdx.x == 0) {
-        unsigned long long t;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        probe[blockIdx.x * kProbeSlots + slot] = t;
+    if (probe != nullptr) {  // (callers are warp-uniform)
+        if (threadIdx.x == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            probe[blockIdx.x * kProbeSlots + slot] = t;
+        }
+        __syncwarp();  // reconverge: a diverged warp would take the collectives' slow path
     }
 }
 
@@ -191,7 +197,10 @@ template <int D, int G>
 struct Layout {
     static constexpr int NROW = (G == 1) ? 1 : 2;    // metadata rows staged per channel
     static constexpr int PPC = (G == 1) ? 512 : 256;  // pages per estimate chunk
-    static constexpr size_t stage_bytes = size_t(NROW) * D * PPC * 2;
+    // GQA: the metadata stage; MHA: the channel-group partial sums [8][512] (fp64) and the
+    // tail rows [D][kTail].
+    static constexpr size_t stage_bytes =
+        (G == 1) ? size_t(8) * kThreads * 8 + size_t(D) * kTail * 2 : size_t(NROW) * D * PPC * 2;
     static constexpr size_t scratch_bytes =
         kSelGroups * sizeof(SelectScratch<kSelThreads>) + sizeof(SelectScratch<kThreads>);
     static size_t region_a(uint32_t pmax) {
@@ -253,7 +262,10 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
     asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
     // Everything below reads data earlier kernels wrote.
     stamp(p.probe, 0);
-    if (p.probe && tid == 0) p.probe[blockIdx.x * kProbeSlots + 24] = clock64();
+    if (p.probe) {
+        if (tid == 0) p.probe[blockIdx.x * kProbeSlots + 24] = clock64();
+        __syncwarp();
+    }
     asm volatile("griddepcontrol.wait;" ::: "memory");
     stamp(p.probe, 1);
 
@@ -434,7 +446,6 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
         // passes is staged with cp.async at the start and finished after the last pass, so
         // it costs no extra round trip.
         constexpr int CPG = D / 8;  // channels per warp
-        constexpr uint32_t kTail = 64;
         const int cg = warp & 7, half = warp >> 3;
         double* part = reinterpret_cast<double*>(smem);               // [8][512] (region A)
         __half* tstage = reinterpret_cast<__half*>(part + 8 * kThreads);  // [D][kTail]
@@ -899,7 +910,10 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
         __syncthreads();
     }
     stamp(p.probe, 19);
-    if (p.probe && tid == 0) p.probe[blockIdx.x * kProbeSlots + 25] = clock64();
+    if (p.probe) {
+        if (tid == 0) p.probe[blockIdx.x * kProbeSlots + 25] = clock64();
+        __syncwarp();
+    }
 
     // Rank 0: merge the C partials of every head in rank order: weights
     // w_r = exp2(m_r - M) / L (every thread computes its head's C weights itself), then
@@ -929,10 +943,13 @@ int run_fused(qk_cache* c, FusedParams prm, uint32_t batch, uint32_t cluster,
               uint32_t max_pages, cudaStream_t st) {
     using LY = Layout<D, G>;
     // Selection keys of every head exchanged through the cluster's shared memory when they
-    // fit (max_pages bounds the candidates of this launch; graph replays that outgrow it
-    // take the HBM path inside the kernel).
-    const uint32_t cap = (key_slots(max_pages) + 1) & ~1u;  // even: 16-byte aligned rows
-    prm.key_cap = (size_t(G) * cap * 8 <= kKeysBudget) ? cap : 0u;
+    // fit.  The key array is sized for the cache's capacity (within the budget), not for
+    // this launch's pages: a CUDA graph captured now replays on longer contexts, and a
+    // launch whose candidates outgrow the array takes the HBM path inside the kernel.
+    const uint32_t budget_slots = uint32_t(keys_budget(G) / (size_t(G) * 8)) & ~1u;
+    const uint32_t full_slots = (key_slots(c->Pmax) + 1) & ~1u;  // even: 16-byte aligned rows
+    const uint32_t cap = full_slots < budget_slots ? full_slots : budget_slots;
+    prm.key_cap = key_slots(max_pages) <= cap ? cap : 0u;
     const size_t region_a = LY::region_a(c->Pmax);
     size_t smem = LY::bytes(c->Pmax, prm.key_cap, cluster);
     while (smem > kMaxSmem && cluster > 1) {  // large GQA groups: fewer partial slots

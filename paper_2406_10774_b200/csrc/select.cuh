@@ -24,10 +24,13 @@ namespace qk {
 
 // Optional phase stamps (QK_PROBE): slots 11..15 of the per-CTA record (decode.cu).
 __device__ __forceinline__ void sel_stamp(unsigned long long* probe, int slot) {
-    if (probe != nullptr && threadIdx.x == 0) {
-        unsigned long long t;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        probe[blockIdx.x * kProbeSlots + slot] = t;
+    if (probe != nullptr) {  // (callers are warp-uniform)
+        if (threadIdx.x == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            probe[blockIdx.x * kProbeSlots + slot] = t;
+        }
+        __syncwarp();  // reconverge: a diverged warp would take the collectives' slow path
     }
 }
 

@@ -24,6 +24,8 @@ ap.add_argument("--kv-heads", type=int, default=None)
 ap.add_argument("--batch", type=int, default=1)
 ap.add_argument("--layers", type=int, default=4)
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--graph-steps", type=int, default=1, help="graph mode: replays before the measured one")
+ap.add_argument("--fresh-q", action="store_true", help="graph mode: new random q/k/v per replay (as bench.py)")
 args = ap.parse_args()
 H, D, S = args.heads, 128, 16
 Hkv = args.kv_heads or H
@@ -93,10 +95,23 @@ if os.environ.get("QK_PROBE_GRAPH"):
     for _ in range(3):
         g2.replay()
     s.synchronize()
-    lib.qk_debug_probe(qc._h, buf.ctypes.data, buf.size, None)  # clear
-    big = np.zeros(n * args.layers, dtype=np.uint64)
-    g2.replay()
+    qs = (torch.randn((args.graph_steps + 1, args.batch, H, D), generator=g, device=dev) / D ** 0.5).half()
+    ks = (torch.randn((args.graph_steps + 1, args.batch, Hkv, D), generator=g, device=dev) / D ** 0.5).half()
+    t_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    with torch.cuda.stream(s):
+        for i in range(args.graph_steps):
+            if args.fresh_q:
+                qb.copy_(qs[i], non_blocking=True)
+                kb.copy_(ks[i], non_blocking=True)
+            if i == args.graph_steps - 1:
+                s.synchronize()
+                lib.qk_debug_probe(qc._h, buf.ctypes.data, buf.size, None)  # clear
+                t_ev[0].record(s)
+            g2.replay()
+        t_ev[1].record(s)
     s.synchronize()
+    print(json.dumps({"last_replay_event_us_per_layer": round(t_ev[0].elapsed_time(t_ev[1]) * 1e3 / args.layers, 2)}))
+    big = np.zeros(n * args.layers, dtype=np.uint64)
     lib.qk_debug_probe(qc._h, big.ctypes.data, big.size, None)
     per = big.reshape(args.layers, -1, SLOTS).astype(np.int64)
     prev_end = None
