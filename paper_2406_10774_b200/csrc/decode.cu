@@ -267,6 +267,9 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
         __syncwarp();
     }
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    // The next kernel may launch now: its CTAs take idle SMs and block in their own
+    // griddepcontrol.wait until this grid has completed (hides the launch latency).
+    asm volatile("griddepcontrol.launch_dependents;");
     stamp(p.probe, 1);
 
     // The length and the query are independent loads: issue both before either is used.
@@ -902,7 +905,6 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
         }
         __syncthreads();  // s_o / s_m reused by the next head; partials issued
     }
-    asm volatile("griddepcontrol.launch_dependents;");
     stamp(p.probe, 18);
     if (C > 1 && rank != 0) return;  // the partials complete on rank 0's merge_bar
     if (C > 1) {
