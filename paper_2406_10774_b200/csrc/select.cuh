@@ -44,6 +44,7 @@ struct SelectScratch {
     unsigned int cand_idx[32];
     alignas(16) unsigned long long cand2[66];  // (key, index) pairs of the threshold bin + trash
     unsigned int cand_take[33];
+    unsigned int selbits[NT / 2];  // block_select_reg: boundary-bin verdicts, 1 bit per key (KPT <= 16)
     int trash_out;
     // Early-signal of block_select_reg: after the first radix pass every key whose top
     // 11 bits (after the common prefix `sig_shift`) exceed `sig_bin` is selected.
@@ -573,9 +574,11 @@ __device__ void block_select_reg(const unsigned long long (&key)[KPT], uint32_t 
     const int nv = n > i0 ? int(min(uint32_t(KPT), n - i0)) : 0;  // valid keys of this thread
     uint4* hist4 = reinterpret_cast<uint4*>(sc.hist);
 
+    static_assert(KPT <= 16, "selbits holds 16 keys per thread");
 #pragma unroll
     for (int j = 0; j < BPL / 4; ++j) hist4[gt * (BPL / 4) + j] = make_uint4(0, 0, 0, 0);
     if (gt == 0) sc.n_cand = 0;
+    if (gt < NT / 2) sc.selbits[gt] = 0u;
     unsigned long long dx = 0;
 #pragma unroll
     for (int j = 0; j < KPT; ++j)
@@ -646,35 +649,31 @@ __device__ void block_select_reg(const unsigned long long (&key)[KPT], uint32_t 
         return;
     }
     // Keys above the bin are in; keys of the bin by TAKE_BIN or by rank (<= 32 keys).
-    const unsigned int lt_mask = (1u << lane) - 1u;
-    bool take[KPT];
+    // Per-thread 16-bit masks keep the register footprint small (the per-key arrays of an
+    // earlier form serialised warp 0's ranking loads).
+    unsigned int takem = 0, candm = 0;
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) {
+        const unsigned int d = h[j] >> 21;
+        takem |= (j < nv && d > bin) ? 1u << j : 0u;
+        candm |= (j < nv && d == bin) ? 1u << j : 0u;
+    }
     if (bin_count == krem) {
-#pragma unroll
-        for (int j = 0; j < KPT; ++j) take[j] = j < nv && (h[j] >> 21) >= bin;
+        takem |= candm;
     } else {
-        // Gather the bin's keys: slots from ballots (one atomic per warp), stores branch
-        // free (non-candidates write the trash slot 32).
-        unsigned int cm[KPT], wtot = 0;
-#pragma unroll
-        for (int j = 0; j < KPT; ++j) {
-            cm[j] = __ballot_sync(0xffffffffu, j < nv && (h[j] >> 21) == bin);
-            wtot += __popc(cm[j]);
-        }
+        // Gather the bin's keys: warp-scanned slots, one shared atomic per warp.
+        const unsigned int cnt = __popc(candm);
+        const unsigned int incl_c = warp_incl_scan(cnt);
         unsigned int base = 0;
-        if (lane == 0 && wtot) base = atomicAdd(&sc.n_cand, wtot);
-        base = __shfl_sync(0xffffffffu, base, 0);
-        unsigned int slot[KPT];
+        if (lane == 31 && incl_c) base = atomicAdd(&sc.n_cand, incl_c);
+        base = __shfl_sync(0xffffffffu, base, 31) + incl_c - cnt;
 #pragma unroll
-        for (int j = 0; j < KPT; ++j) {
-            const bool mine = (cm[j] >> lane) & 1u;
-            slot[j] = mine ? base + __popc(cm[j] & lt_mask) : 32u;
-            base += __popc(cm[j]);
-            reinterpret_cast<ulonglong2*>(sc.cand2)[slot[j]] = make_ulonglong2(key[j], i0 + j);
-            take[j] = j < nv && (h[j] >> 21) > bin;
+        for (int j = 0; j < KPT; ++j) {  // static indices keep key[] in registers
+            if ((candm >> j) & 1u) reinterpret_cast<ulonglong2*>(sc.cand2)[base++] = make_ulonglong2(key[j], i0 + j);
         }
         group_sync<NT>(bar);
-        const unsigned int nc = sc.n_cand;
-        if (warp == 0) {  // lane m ranks candidate m, straight-line
+        if (warp == 0) {  // lane m ranks candidate m; verdicts go to the key bitmap
+            const unsigned int nc = sc.n_cand;
             const ulonglong2 me = reinterpret_cast<const ulonglong2*>(sc.cand2)[lane];
             unsigned int rank = 0;
 #pragma unroll
@@ -682,27 +681,21 @@ __device__ void block_select_reg(const unsigned long long (&key)[KPT], uint32_t 
                 const ulonglong2 o = reinterpret_cast<const ulonglong2*>(sc.cand2)[m];
                 rank += (uint32_t(m) < nc) & ((o.x > me.x) | ((o.x == me.x) & (o.y < me.y)));
             }
-            sc.cand_take[lane] = rank < krem;
-            if (lane == 0) sc.cand_take[32] = 0u;
+            if (uint32_t(lane) < nc && rank < krem) {
+                const uint32_t idx = uint32_t(me.y);
+                atomicOr(&sc.selbits[idx >> 5], 1u << (idx & 31));
+            }
         }
         group_sync<NT>(bar);
-#pragma unroll
-        for (int j = 0; j < KPT; ++j) take[j] = take[j] | (sc.cand_take[slot[j]] != 0u);
+        takem |= candm & (sc.selbits[i0 >> 5] >> (i0 & 31));
     }
     sel_stamp(probe, 14);
-    unsigned int mine = 0;
-#pragma unroll
-    for (int j = 0; j < KPT; ++j) mine += take[j];
+    const unsigned int mine = __popc(takem);
     const unsigned int incl2 = warp_incl_scan(mine);
     if (lane == 31) sc.warp_sum[warp] = incl2;
     group_sync<NT>(bar);
     unsigned int pos = sum_below<NW>(sc.warp_sum, warp) + incl2 - mine;
-#pragma unroll
-    for (int j = 0; j < KPT; ++j) {  // branch free: rejected keys write a trash word
-        OutT* dst = take[j] ? out + pos : reinterpret_cast<OutT*>(&sc.trash_out);
-        *dst = static_cast<OutT>(i0 + j);
-        pos += take[j];
-    }
+    for (unsigned int m = takem; m; m &= m - 1) out[pos++] = static_cast<OutT>(i0 + uint32_t(__ffs(m) - 1));
     sel_stamp(probe, 15);
 }
 

@@ -15,7 +15,7 @@ constexpr int GT = 128;  // selection group
 
 __global__ void __launch_bounds__(NT, 1) sel_kernel(const double* __restrict__ scores, int n,
                                                    int target, int* out_pages,
-                                                   long long* cyc) {
+                                                   long long* cyc, unsigned long long* probe) {
     extern __shared__ unsigned long long keys[];
     __shared__ SelectScratch<NT> sc;
     __shared__ SelectScratch<GT> sg;
@@ -53,6 +53,15 @@ __global__ void __launch_bounds__(NT, 1) sel_kernel(const double* __restrict__ s
         }
         d = clock64();
         d = c + (d - c) / 10;
+        // one more call with globaltimer stamps (slots 10 = start, 11 bin, 14 take, 15 done)
+        if (gt == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            probe[blockIdx.x * 32 + 10] = t;
+        }
+        group_sync<GT>(1);
+        block_select_reg<GT, 16>(k16, n, target, ref, list, sg, gt, 1, probe);
+        group_sync<GT>(1);
         e0 = clock64();
         block_select_reg_wide<GT, 16>(k16, n, target, ref, list, sg, gt, 1, nullptr, trace);
         group_sync<GT>(1);
@@ -79,6 +88,9 @@ int main(int argc, char** argv) {
     double* d;
     int* pages;
     long long* cyc;
+    unsigned long long* probe;
+    cudaMalloc(&probe, 128 * 32 * 8);
+    cudaMemset(probe, 0, 128 * 32 * 8);
     cudaMalloc(&d, size_t(ctas) * n * 8);
     cudaMalloc(&pages, ctas * 1024 * 4);
     cudaMalloc(&cyc, ctas * 16 * 8);
@@ -86,7 +98,7 @@ int main(int argc, char** argv) {
     const int kpt = (n + NT - 1) / NT;
     const size_t smem = size_t(NT) * (kpt + 1) * 8;
     for (int rep = 0; rep < 3; ++rep) {
-        sel_kernel<<<ctas, NT, smem>>>(d, n, target, pages, cyc);
+        sel_kernel<<<ctas, NT, smem>>>(d, n, target, pages, cyc, probe);
         cudaDeviceSynchronize();
     }
     long long c[16 * 128];
@@ -104,6 +116,20 @@ int main(int argc, char** argv) {
         double a = 0;
         for (int i = 0; i < ctas; ++i) a += c[16 * i + k];
         printf("%-22s %7.0f cycles\n", names[k], a / ctas);
+    }
+    unsigned long long pr[128 * 32];
+    cudaMemcpy(pr, probe, sizeof(pr), cudaMemcpyDeviceToHost);
+    double s11 = 0, s14 = 0, s15 = 0;
+    for (int i = 0; i < ctas; ++i) {
+        s11 += double(pr[i * 32 + 11] - pr[i * 32 + 10]);
+        s14 += double(pr[i * 32 + 14] - pr[i * 32 + 10]);
+        s15 += double(pr[i * 32 + 15] - pr[i * 32 + 10]);
+    }
+    printf("stamps (ns from start): bin known %.0f, take known %.0f, done %.0f\n", s11 / ctas, s14 / ctas, s15 / ctas);
+    for (int k = 24; k < 30; ++k) {
+        double a = 0; int cnt = 0;
+        for (int i = 0; i < ctas; ++i) if (pr[i * 32 + k]) { a += double(pr[i * 32 + k] - pr[i * 32 + 10]); ++cnt; }
+        printf("  slot %d: %d ctas, %.0f ns\n", k, cnt, cnt ? a / cnt : 0.0);
     }
     printf("(%s)\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
