@@ -81,6 +81,18 @@ for rep in range(args.reps):
         res.append(row)
 for r in res[-args.layers:]:
     print(json.dumps(r))
+if os.environ.get("QK_PROBE_RANKS"):
+    # Per cluster rank (CTA index % cluster size): median stamp of the last layer's CTAs.
+    t = buf[(args.layers - 1) * n:args.layers * n].reshape(-1, SLOTS).astype(np.int64)
+    idx = np.nonzero(t[:, 0] > 0)[0]
+    t = t[idx]
+    t0 = t[:, 0].min()
+    C = int(os.environ.get("QK_PROBE_RANKS"))
+    for k in (3, 5, 6, 7, 8, 9, 10, 16, 17, 18):
+        col = (t[:, k] - t0) / 1000.0
+        print(json.dumps({"stamp": names.get(k, k), **{f"rank{r}": round(float(np.median(col[idx % C == r])), 2)
+                                                        for r in range(C)},
+                          "max_rank": int(np.argmax([np.max(col[idx % C == r]) for r in range(C)]))}))
 
 # ---- graph mode: inter-kernel gaps of a CUDA graph of every layer (as bench.py runs) ----
 if os.environ.get("QK_PROBE_GRAPH"):
