@@ -23,16 +23,26 @@
 namespace qk {
 
 // Optional phase stamps (QK_PROBE): slots 11..15 of the per-CTA record (decode.cu).
+// QK_SEL_CYCLES (microbenchmarks only) records clock64 instead and enables fine stamps.
 __device__ __forceinline__ void sel_stamp(unsigned long long* probe, int slot) {
     if (probe != nullptr) {  // (callers are warp-uniform)
         if (threadIdx.x == 0) {
             unsigned long long t;
+#ifdef QK_SEL_CYCLES
+            t = clock64();
+#else
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+#endif
             probe[blockIdx.x * kProbeSlots + slot] = t;
         }
         __syncwarp();  // reconverge: a diverged warp would take the collectives' slow path
     }
 }
+#ifdef QK_SEL_CYCLES
+#define QK_SEL_FINE(probe, slot) sel_stamp(probe, slot)
+#else
+#define QK_SEL_FINE(probe, slot) ((void)0)
+#endif
 
 template <int NT>
 struct SelectScratch {
@@ -589,6 +599,7 @@ __device__ void block_select_reg(const unsigned long long (&key)[KPT], uint32_t 
         if (lane == 0) sc.red_max[warp] = (static_cast<unsigned long long>(dhi) << 32) | dlo;
     }
     group_sync<NT>(bar);
+    QK_SEL_FINE(probe, 20);
     unsigned long long diff = 0;
 #pragma unroll
     for (int w2 = 0; w2 < NW / 2; ++w2) {
@@ -609,7 +620,9 @@ __device__ void block_select_reg(const unsigned long long (&key)[KPT], uint32_t 
         // Branch-free: invalid entries count into the trash bin 2048.
         atomicAdd(&sc.hist[j < nv ? (h[j] >> 21) : 2048u], 1u);
     }
+    QK_SEL_FINE(probe, 21);
     group_sync<NT>(bar);
+    QK_SEL_FINE(probe, 22);
     unsigned int c[BPL], sl = 0;
 #pragma unroll
     for (int j4 = 0; j4 < BPL / 4; ++j4) {
@@ -623,6 +636,7 @@ __device__ void block_select_reg(const unsigned long long (&key)[KPT], uint32_t 
     for (int j = 0; j < BPL; ++j) sl += c[j];
     const unsigned int incl = warp_incl_scan(sl);
     if (lane == 31) sc.warp_sum[warp] = incl;
+    QK_SEL_FINE(probe, 23);
     group_sync<NT>(bar);
     {
         unsigned int above = sum_below<NW>(sc.warp_sum, warp) + incl - sl;
@@ -665,27 +679,35 @@ __device__ void block_select_reg(const unsigned long long (&key)[KPT], uint32_t 
         const unsigned int cnt = __popc(candm);
         const unsigned int incl_c = warp_incl_scan(cnt);
         unsigned int base = 0;
-        if (lane == 31 && incl_c) base = atomicAdd(&sc.n_cand, incl_c);
+        if (lane == 31 && incl_c)  // plain atom (the intrinsic gets a warp-aggregation prologue)
+            asm volatile("atom.shared.add.u32 %0, [%1], %2;"
+                         : "=r"(base)
+                         : "r"(static_cast<unsigned int>(__cvta_generic_to_shared(&sc.n_cand))), "r"(incl_c)
+                         : "memory");
         base = __shfl_sync(0xffffffffu, base, 31) + incl_c - cnt;
 #pragma unroll
         for (int j = 0; j < KPT; ++j) {  // static indices keep key[] in registers
             if ((candm >> j) & 1u) reinterpret_cast<ulonglong2*>(sc.cand2)[base++] = make_ulonglong2(key[j], i0 + j);
         }
+        QK_SEL_FINE(probe, 24);
         group_sync<NT>(bar);
+        QK_SEL_FINE(probe, 25);
         if (warp == 0) {  // lane m ranks candidate m; verdicts go to the key bitmap
             const unsigned int nc = sc.n_cand;
             const ulonglong2 me = reinterpret_cast<const ulonglong2*>(sc.cand2)[lane];
             unsigned int rank = 0;
-#pragma unroll
-            for (int m = 0; m < 32; ++m) {
+            // Only the nc (<= 32, usually a few) gathered candidates: a warp-uniform trip
+            // count (each iteration is a dependent compare chain of ~50 cycles).
+            for (uint32_t m = 0; m < nc; ++m) {
                 const ulonglong2 o = reinterpret_cast<const ulonglong2*>(sc.cand2)[m];
-                rank += (uint32_t(m) < nc) & ((o.x > me.x) | ((o.x == me.x) & (o.y < me.y)));
+                rank += (o.x > me.x) | ((o.x == me.x) & (o.y < me.y));
             }
             if (uint32_t(lane) < nc && rank < krem) {
                 const uint32_t idx = uint32_t(me.y);
                 atomicOr(&sc.selbits[idx >> 5], 1u << (idx & 31));
             }
         }
+        QK_SEL_FINE(probe, 26);
         group_sync<NT>(bar);
         takem |= candm & (sc.selbits[i0 >> 5] >> (i0 & 31));
     }
@@ -693,6 +715,7 @@ __device__ void block_select_reg(const unsigned long long (&key)[KPT], uint32_t 
     const unsigned int mine = __popc(takem);
     const unsigned int incl2 = warp_incl_scan(mine);
     if (lane == 31) sc.warp_sum[warp] = incl2;
+    QK_SEL_FINE(probe, 27);
     group_sync<NT>(bar);
     unsigned int pos = sum_below<NW>(sc.warp_sum, warp) + incl2 - mine;
     for (unsigned int m = takem; m; m &= m - 1) out[pos++] = static_cast<OutT>(i0 + uint32_t(__ffs(m) - 1));

@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(NT, 1) sel_kernel(const double* __restrict__ s
         // one more call with globaltimer stamps (slots 10 = start, 11 bin, 14 take, 15 done)
         if (gt == 0) {
             unsigned long long t;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            t = clock64();
             probe[blockIdx.x * 32 + 10] = t;
         }
         group_sync<GT>(1);
@@ -125,7 +125,14 @@ int main(int argc, char** argv) {
         s14 += double(pr[i * 32 + 14] - pr[i * 32 + 10]);
         s15 += double(pr[i * 32 + 15] - pr[i * 32 + 10]);
     }
-    printf("stamps (ns from start): bin known %.0f, take known %.0f, done %.0f\n", s11 / ctas, s14 / ctas, s15 / ctas);
+    printf("stamps (cycles from start): bin known %.0f, take known %.0f, done %.0f\n", s11 / ctas, s14 / ctas, s15 / ctas);
+    const int order[] = {20, 21, 22, 23, 11, 24, 25, 26, 14, 27, 15};
+    const char* nm[] = {"ordiff synced", "hist issued", "hist synced", "scan done", "bin known", "gathered", "gather synced", "ranked", "take known", "compaction scan", "done"};
+    for (int q = 0; q < 11; ++q) {
+        double a = 0; int cnt = 0;
+        for (int i = 0; i < ctas; ++i) if (pr[i * 32 + order[q]] > pr[i * 32 + 10]) { a += double(pr[i * 32 + order[q]] - pr[i * 32 + 10]); ++cnt; }
+        printf("  %-16s %4d ctas %7.0f cycles\n", nm[q], cnt, cnt ? a / cnt : 0.0);
+    }
     for (int k = 24; k < 30; ++k) {
         double a = 0; int cnt = 0;
         for (int i = 0; i < ctas; ++i) if (pr[i * 32 + k]) { a += double(pr[i * 32 + k] - pr[i * 32 + 10]); ++cnt; }
