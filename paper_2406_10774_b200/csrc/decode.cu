@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
     unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem + region_a_bytes);
     double* dq = reinterpret_cast<double*>(keys + size_t(G) * p.key_cap);  // [G][D]
     int32_t* sel = reinterpret_cast<int32_t*>(dq + G * D);                 // [G][kMaxFusedK]
-    float* parts = reinterpret_cast<float*>(sel + G * kMaxFusedK);        // [G][C][D+2]
+    float* parts = reinterpret_cast<float*>(sel + G * kMaxFusedK);        // [G][D+2][C]
     unsigned long long* mbar = reinterpret_cast<unsigned long long*>(
         (reinterpret_cast<uintptr_t>(parts + size_t(G) * C * (D + 2)) + 7) & ~uintptr_t(7));
     __shared__ unsigned char need[D];
@@ -887,19 +887,21 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
                 L += __shfl_sync(0xffffffffu, myl, w);
                 acc += s_o[w][tid] * __shfl_sync(0xffffffffu, myw, w);
             }
-            float* slot = parts + (size_t(g) * C + rank) * (D + 2);
+            // Partials layout [g][D+2][C] (element-major): rank 0 reads each element of the
+            // C ranks as one vector.
+            float* hbase = parts + size_t(g) * (D + 2) * C;
             if (C == 1 || rank == 0) {
-                slot[2 + tid] = acc;
+                hbase[(2 + tid) * C + rank] = acc;
                 if (tid == 0) {
-                    slot[0] = M;
-                    slot[1] = L;
+                    hbase[rank] = M;
+                    hbase[C + rank] = L;
                 }
             } else {
                 const uint32_t rb = map_rank(merge_bar, 0);
-                st_async_f32(map_rank(slot + 2 + tid, 0), acc, rb);
+                st_async_f32(map_rank(hbase + (2 + tid) * C + rank, 0), acc, rb);
                 if (tid == 0) {
-                    st_async_f32(map_rank(slot, 0), M, rb);
-                    st_async_f32(map_rank(slot + 1, 0), L, rb);
+                    st_async_f32(map_rank(hbase + rank, 0), M, rb);
+                    st_async_f32(map_rank(hbase + C + rank, 0), L, rb);
                 }
             }
         }
@@ -923,15 +925,30 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
     for (int i = tid; i < G * int(p.head_dim); i += kThreads) {
         const int g = i / int(p.head_dim), d = i % int(p.head_dim);
         const size_t bh = size_t(b) * Hq + size_t(kvh) * G + g;
-        const float* hb = parts + size_t(g) * C * (D + 2);
-        float Mg = -CUDART_INF_F;
-        for (uint32_t r = 0; r < C; ++r) Mg = fmaxf(Mg, hb[r * (D + 2)]);
+        const float* hb = parts + size_t(g) * (D + 2) * C;  // [D+2][C]
         float Lg = 0.0f, acc = 0.0f;
-        for (uint32_t r = 0; r < C; ++r) {
-            const float mr = hb[r * (D + 2)];
-            const float w = (mr == -CUDART_INF_F) ? 0.0f : exp2f(mr - Mg);
-            Lg = fmaf(hb[r * (D + 2) + 1], w, Lg);
-            acc = fmaf(hb[r * (D + 2) + 2 + d], w, acc);
+        if (C == 4) {  // the common cluster: one vector per element
+            const float4 m4 = reinterpret_cast<const float4*>(hb)[0];
+            const float4 l4 = reinterpret_cast<const float4*>(hb)[1];
+            const float4 o4 = reinterpret_cast<const float4*>(hb)[2 + d];
+            const float mr[4] = {m4.x, m4.y, m4.z, m4.w}, lr[4] = {l4.x, l4.y, l4.z, l4.w},
+                        orr[4] = {o4.x, o4.y, o4.z, o4.w};
+            const float Mg = fmaxf(fmaxf(mr[0], mr[1]), fmaxf(mr[2], mr[3]));
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {  // rank order, as the generic path
+                const float w = (mr[r] == -CUDART_INF_F) ? 0.0f : exp2f(mr[r] - Mg);
+                Lg = fmaf(lr[r], w, Lg);
+                acc = fmaf(orr[r], w, acc);
+            }
+        } else {
+            float Mg = -CUDART_INF_F;
+            for (uint32_t r = 0; r < C; ++r) Mg = fmaxf(Mg, hb[r]);
+            for (uint32_t r = 0; r < C; ++r) {
+                const float mr = hb[r];
+                const float w = (mr == -CUDART_INF_F) ? 0.0f : exp2f(mr - Mg);
+                Lg = fmaf(hb[C + r], w, Lg);
+                acc = fmaf(hb[(2 + d) * C + r], w, acc);
+            }
         }
         acc = acc / Lg;
         if (p.out_dtype == QK_DTYPE_F32) static_cast<float*>(p.out)[bh * p.head_dim + d] = acc;
