@@ -204,3 +204,46 @@ def test_fused_step_graph_replay(qk, oracle_c):
         assert torch.equal(out_g, ref), i
     graphed.qc.sync_lengths()
     assert graphed.qc.token_count(0, 0) == L + 4 == eager.qc.token_count(0, 0)
+
+
+def test_fused_graph_replay_outgrows_capture(qk, oracle_c):
+    """A graph captured at 2047 pages replayed while the context grows past 2048 pages
+    (per-CTA tail pass, 256-thread selection group): every replay equals the eager step
+    bitwise, and the last one matches the oracle.  Guards the shared-memory key array
+    being sized for the cache, not for the capture-time page count."""
+    rng = np.random.default_rng(11)
+    B, H, d, S, L, steps = 1, 4, 128, 16, 2047 * 16 - 4, 40
+    eager = Layer(qk, np.random.default_rng(3), B, H, H, d, S, [L], extra=steps + 8)
+    graphed = Layer(qk, np.random.default_rng(3), B, H, H, d, S, [L], extra=steps + 8)
+    sd = 1 / np.sqrt(d)
+    qs = [half(rng.standard_normal((B, H, d)) * sd) for _ in range(steps)]
+    ks = [half(rng.standard_normal((B, H, d)) * sd) for _ in range(steps)]
+    vs = [half(rng.standard_normal((B, H, d)) * sd) for _ in range(steps)]
+    t = lambda a: torch.from_numpy(a).half().cuda()  # noqa: E731
+    qb, kb, vb = t(qs[0]), t(ks[0]), t(vs[0])
+    out_g = torch.zeros((B, H, d), dtype=torch.float32, device="cuda")
+    s = torch.cuda.Stream()
+    warm = Layer(qk, np.random.default_rng(2), B, H, H, d, S, [16])
+    warm.qc.decode_step(0, qb, kb, vb, 2048, stream=s)  # load the kernel before capture
+    s.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        graphed.qc.decode_step(0, qb, kb, vb, 2048, out=out_g, stream=s)
+    for i in range(steps):
+        with torch.cuda.stream(s):
+            qb.copy_(t(qs[i]))
+            kb.copy_(t(ks[i]))
+            vb.copy_(t(vs[i]))
+            g.replay()
+        s.synchronize()
+        ref = eager.qc.decode_step(0, t(qs[i]), t(ks[i]), t(vs[i]), 2048)
+        assert torch.equal(out_g, ref), i
+        eager.keys[0] = np.concatenate([eager.keys[0], ks[i][0][:, None]], axis=1)
+        eager.vals[0] = np.concatenate([eager.vals[0], vs[i][0][:, None]], axis=1)
+    graphed.qc.sync_lengths()
+    assert graphed.qc.token_count(0, 0) == L + steps  # 2050 pages at the end
+    out = out_g.cpu().numpy()
+    for h in range(H):
+        _, _, o_want = oracle_c.quest_step(qs[-1][0, h], eager.keys[0][h], eager.vals[0][h], S,
+                                           2048, True, True)
+        assert rel_l2(out[0, h], o_want) <= TOL, h
