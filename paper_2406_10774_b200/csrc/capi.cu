@@ -3,6 +3,7 @@
 // No exception crosses this boundary; every failure is a status code plus a
 // thread-local message.
 #include <cmath>
+#include <chrono>
 #include <cstring>
 #include <new>
 #include <string>
@@ -80,7 +81,7 @@ void free_cache(qk_cache* c) {
     void* ptrs[] = {c->k_pool,    c->v_pool,    c->meta,      c->d_len,     c->ws_partial,
                     c->ws_ticket, c->d_status,  c->ws_scores, c->ws_pages,  c->ws_counts,
                     c->ws_io,     c->ws_out,    c->len_ticket, c->probe,     c->ws_lse,
-                    c->prange};
+                    c->prange,    c->done_counter};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->host_stage) cudaFreeHost(c->host_stage);
@@ -494,16 +495,20 @@ int qk_decode_step_host(qk_cache* c, uint32_t layer, const uint16_t* q_host,
     const size_t out_max = size_t(c->B) * c->Hq * hd * 4;
     if (!c->host_stage) {
         void* h = nullptr;
-        int rc = cuda_check(cudaHostAlloc(&h, in_max + out_max, cudaHostAllocMapped), "cudaHostAlloc");
+        int rc = cuda_check(cudaHostAlloc(&h, in_max + out_max + 64, cudaHostAllocMapped), "cudaHostAlloc");
         if (rc) return rc;
         void* d = nullptr;
         rc = cuda_check(cudaHostGetDevicePointer(&d, h, 0), "cudaHostGetDevicePointer");
+        if (!rc) rc = cuda_check(cudaMalloc(&c->done_counter, sizeof(uint32_t)), "cudaMalloc done");
+        if (!rc) rc = cuda_check(cudaMemset(c->done_counter, 0, sizeof(uint32_t)), "cudaMemset done");
         if (rc) {
             cudaFreeHost(h);
             return rc;
         }
         c->host_stage = static_cast<unsigned char*>(h);
         c->host_stage_dev = static_cast<unsigned char*>(d);
+        c->done_flag_dev = reinterpret_cast<uint32_t*>(c->host_stage_dev + in_max + out_max);
+        *reinterpret_cast<volatile uint32_t*>(c->host_stage + in_max + out_max) = 0;
     }
     uint16_t* hq = reinterpret_cast<uint16_t*>(c->host_stage);
     std::memcpy(hq, q_host, nq * 2);
@@ -513,9 +518,32 @@ int qk_decode_step_host(qk_cache* c, uint32_t layer, const uint16_t* q_host,
     }
     const uint16_t* dq = reinterpret_cast<const uint16_t*>(c->host_stage_dev);
     float* dout = reinterpret_cast<float*>(c->host_stage_dev + in_max);
+    // Completion: the fused kernel's last unit publishes `seq` in the mapped word, so the host
+    // spins on it (~1 us after the last output lands) instead of synchronising the stream.
+    // Paths that do not consume the request (unfused fallback) synchronise as before.
+    const uint32_t seq = ++c->done_seq;
+    c->pending_done_flag = c->done_flag_dev;
+    c->pending_done_seq = seq;
     int rc = qk_decode_step(c, layer, dq, k_host ? dq + nq : nullptr, k_host ? dq + nq + nkv : nullptr,
                             batch, cfg, dout, QK_DTYPE_F32, nullptr, 0, nullptr, stream);
-    if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "qk_decode_step_host");
+    const bool signalled = c->pending_done_flag == nullptr;  // consumed by a fused launch
+    c->pending_done_flag = nullptr;
+    if (!rc && signalled) {
+        const volatile uint32_t* word = reinterpret_cast<volatile uint32_t*>(c->host_stage + in_max + out_max);
+        const auto t0 = std::chrono::steady_clock::now();
+        while (__atomic_load_n(const_cast<const uint32_t*>(word), __ATOMIC_ACQUIRE) != seq) {
+            // A kernel that faults never signals: after a generous wait, let the stream
+            // synchronisation report the error.
+            if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(2)) {
+                rc = cuda_check(cudaStreamSynchronize(st), "qk_decode_step_host");
+                if (!rc && __atomic_load_n(const_cast<const uint32_t*>(word), __ATOMIC_ACQUIRE) != seq)
+                    rc = set_error(QK_ERR_CUDA, "qk_decode_step_host: completion not signalled");
+                break;
+            }
+        }
+    } else if (!rc) {
+        rc = cuda_check(cudaStreamSynchronize(st), "qk_decode_step_host");
+    }
     if (!rc) std::memcpy(out_host, c->host_stage + in_max, size_t(batch) * c->Hq * hd * 4);
     return rc;
 }

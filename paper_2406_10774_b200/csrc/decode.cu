@@ -186,7 +186,21 @@ struct FusedParams {
     int prefetch;         // L2-prefetch certainly-selected pages during the selection
     float scale_log2;
     unsigned long long* probe;  // optional [grid][kProbeSlots] globaltimer stamps
+    uint32_t* done_flag;        // optional host-mapped completion word (host step)
+    uint32_t* done_counter;     // units finished in this launch (reset by the last one)
+    uint32_t done_seq;
 };
+
+// Host-step completion (called by thread 0 of a unit's rank-0 CTA once its outputs are
+// written and ordered by a CTA barrier): the last unit publishes the sequence number with
+// release at system scope, after every unit's fence.
+__device__ __forceinline__ void signal_done(const FusedParams& p, uint32_t units) {
+    __threadfence_system();
+    if (atomicAdd(p.done_counter, 1u) == units - 1) {
+        *p.done_counter = 0;  // for the next launch (ordered by the kernel boundary)
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.done_flag), "r"(p.done_seq) : "memory");
+    }
+}
 
 // Dynamic shared memory:
 //   [region A: metadata stage | after the estimate: selection scratch + padded keys]
@@ -288,6 +302,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
     const size_t s = (size_t(p.layer) * p.B + b) * p.Hkv + kvh;
     if (append && t_old >= p.capacity) {  // host-checked; keep the cache intact
         if (tid == 0 && rank == 0) record_status(p.status, QK_DEV_CAPACITY);
+        if (p.done_flag && tid == 0 && rank == 0) signal_done(p, gridDim.x / C);
         return;  // uniform over the cluster: no barrier is left waiting
     }
 
@@ -954,6 +969,10 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
         if (p.out_dtype == QK_DTYPE_F32) static_cast<float*>(p.out)[bh * p.head_dim + d] = acc;
         else static_cast<__half*>(p.out)[bh * p.head_dim + d] = __float2half_rn(acc);
     }
+    if (p.done_flag) {
+        __syncthreads();  // this unit's outputs are written
+        if (tid == 0) signal_done(p, gridDim.x / C);
+    }
     stamp(p.probe, 20);
 }
 
@@ -1001,7 +1020,8 @@ int run_fused(qk_cache* c, FusedParams prm, uint32_t batch, uint32_t cluster,
     attrs[0].val.clusterDim.y = 1;
     attrs[0].val.clusterDim.z = 1;
     attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attrs[1].val.programmaticStreamSerializationAllowed = getenv("QK_NO_PDL") ? 0 : 1;
+    static const int pdl = getenv("QK_NO_PDL") ? 0 : 1;  // read once (per-launch cost)
+    attrs[1].val.programmaticStreamSerializationAllowed = pdl;
     cfg.attrs = attrs;
     cfg.numAttrs = 2;
     const int rc = cuda_check(cudaLaunchKernelEx(&cfg, kern, prm, uint32_t(region_a)),
@@ -1096,9 +1116,16 @@ int launch_decode(qk_cache* c, uint32_t layer, const __half* q, const __half* k,
     prm.force = cfg.force_include_recent ? 1 : 0;
     prm.out_dtype = out_dtype;
     prm.keep_scores = c->keep_scores ? 1 : 0;
-    prm.prefetch = getenv("QK_NO_PREFETCH") ? 0 : 1;
+    static const int prefetch = getenv("QK_NO_PREFETCH") ? 0 : 1;  // read once
+    prm.prefetch = prefetch;
     prm.scale_log2 = float(1.4426950408889634 / sqrt(double(c->desc.head_dim)));
     prm.probe = c->probe ? c->probe + size_t(layer) * c->B * c->Hkv * kMaxClusterCtas * kProbeSlots : nullptr;
+    if (c->pending_done_flag) {  // the host step asked for a completion word (consumed here)
+        prm.done_flag = c->pending_done_flag;
+        prm.done_counter = c->done_counter;
+        prm.done_seq = c->pending_done_seq;
+        c->pending_done_flag = nullptr;
+    }
     const uint32_t cluster = fused_cluster_size(c, batch, max_pages);
     switch (c->D) {
         case 64: return dispatch_g<64>(c, prm, batch, cluster, max_pages, st);

@@ -73,6 +73,13 @@ struct qk_cache {
     float* ws_lse = nullptr;             // [B][Hq] fp32 (host-buffer entry points)
     unsigned char* host_stage = nullptr; // pinned, device-mapped staging of the host step
     unsigned char* host_stage_dev = nullptr;  // (q, k, v in; fp32 out), allocated lazily
+    // Host-step completion: the last unit of a fused launch writes `seq` into the mapped word
+    // (the host spins on it instead of a stream synchronisation).
+    uint32_t* done_counter = nullptr;    // device: units finished in the current launch
+    uint32_t* done_flag_dev = nullptr;   // device view of the mapped completion word
+    uint32_t done_seq = 0;
+    uint32_t* pending_done_flag = nullptr;  // set by the host step for the next fused launch;
+    uint32_t pending_done_seq = 0;          // launch_decode clears it when it consumes it
     unsigned long long* probe = nullptr; // phase timestamps of the fused kernel (QK_PROBE)
     bool keep_scores = false;            // fused step: estimate every page, keep scores
     uint64_t device_bytes = 0;

@@ -262,3 +262,21 @@ def test_decode_step_host_matches_device(qk):
     out_d = b_.decode_step(0, torch.from_numpy(q).cuda(), torch.from_numpy(kn).cuda(),
                            torch.from_numpy(kn).cuda(), 256)
     assert np.array_equal(out_h, out_d.cpu().numpy())  # same kernel, same inputs
+
+
+def test_decode_step_host_consecutive_steps(qk):
+    """The host step's completion word (the fused kernel's last unit publishes a sequence
+    number the host spins on): eight consecutive host steps, batch 2, GQA 4, each equal to
+    the device step on an identical cache."""
+    rng = np.random.default_rng(8)
+    B, Hq, Hkv, d, S = 2, 8, 2, 128, 16
+    a, _, _ = _layer(qk, np.random.default_rng(9), B, Hq, Hkv, d, S, [3000, 41])
+    b_, _, _ = _layer(qk, np.random.default_rng(9), B, Hq, Hkv, d, S, [3000, 41])
+    for step in range(8):
+        q = half(rng.standard_normal((B, Hq, d)) / np.sqrt(d)).astype(np.float16)
+        kn = half(rng.standard_normal((B, Hkv, d)) / np.sqrt(d)).astype(np.float16)
+        vn = half(rng.standard_normal((B, Hkv, d)) / np.sqrt(d)).astype(np.float16)
+        out_h = a.decode_step_host(0, q, kn, vn, 512)
+        out_d = b_.decode_step(0, torch.from_numpy(q).cuda(), torch.from_numpy(kn).cuda(),
+                               torch.from_numpy(vn).cuda(), 512)
+        assert np.array_equal(out_h, out_d.cpu().numpy()), step
