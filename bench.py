@@ -441,6 +441,7 @@ def run_ours(args):
         "roofline": {
             "bound": "hbm", "achieved": round(achieved_gbs, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved_gbs / peak, 4),
+            "frac_at_8tbs": round(achieved_gbs / 8000.0, 4),  # report both fractions
             "traffic": profiled_traffic() if args.config == "cfg2" else None,
             "kernel": "decode_fused_kernel (one launch = append+estimate+top-K+attend of a layer)",
             "bytes_per_launch": int(bytes_per_layer),
