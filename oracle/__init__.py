@@ -177,7 +177,43 @@ class Reference:
         L.ref_layer_step.argtypes = [ctypes.c_void_p, _f32p, _u32, ctypes.c_int, _u32, _u32, _u32,
                                      ctypes.POINTER(ctypes.c_double),
                                      ctypes.POINTER(ctypes.c_double), _f64p]
+        L.ref_write_trace.argtypes = [ctypes.c_char_p, _u32, _u32, _f32p, _f32p, _f32p]
+        L.ref_read_trace.argtypes = [ctypes.c_char_p, ctypes.POINTER(_u32), ctypes.POINTER(_u32),
+                                     _f32p, _f32p, _f32p, _u32]
+        L.ref_recall_at_n.argtypes = [_u32p, _u32, _f32p, _f32p, _f32p, _u32, _u32, _u32, _u32,
+                                      ctypes.POINTER(ctypes.c_double)]
         self.lib = L
+
+    def write_trace(self, path, keys, values, queries):
+        """The reference's write_trace (workloads.cpp) of float32 [n, d] arrays."""
+        k, v, q = (np.ascontiguousarray(a, np.float32) for a in (keys, values, queries))
+        n, d = k.shape
+        _raise(self.lib.ref_write_trace(str(path).encode(), d, n, k, v,
+                                        q), "write_trace")
+
+    def read_trace(self, path, cap=1 << 16):
+        """The reference's read_trace: (head_dim, keys, values, queries); raises ValueError
+        on trace_format_error (status 4)."""
+        d, n = _u32(0), _u32(0)
+        e = np.zeros(0, np.float32)
+        st = self.lib.ref_read_trace(str(path).encode(), ctypes.byref(d), ctypes.byref(n), e, e, e, 0)
+        if st:
+            raise ValueError(f"read_trace: status {st}")
+        k = np.zeros((n.value, d.value), np.float32)
+        v, q = np.zeros_like(k), np.zeros_like(k)
+        _raise(self.lib.ref_read_trace(str(path).encode(), ctypes.byref(d), ctypes.byref(n), k,
+                                       v, q, n.value), "read_trace")
+        return d.value, k, v, q
+
+    def recall_at_n(self, selected, query, keys, values, page_size, top_n):
+        sel = np.ascontiguousarray(selected, np.uint32)
+        k, v = np.ascontiguousarray(keys, np.float32), np.ascontiguousarray(values, np.float32)
+        q = np.ascontiguousarray(query, np.float32)
+        r = ctypes.c_double(0.0)
+        _raise(self.lib.ref_recall_at_n(sel, len(sel), q, k, v,
+                                        k.shape[0], k.shape[1], page_size, top_n, ctypes.byref(r)),
+               "recall_at_n")
+        return r.value
 
     def validate_config(self, head_dim, page_size, bpe=2):
         _raise(self.lib.ref_validate_config(head_dim, page_size, bpe), "CacheConfig")

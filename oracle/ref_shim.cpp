@@ -8,8 +8,10 @@
 // (kv_store.hpp, criticality.hpp, attention.hpp, reference.hpp, parallel.hpp), mapping
 // exceptions to status codes (invalid_argument -> 1, out_of_range -> 2).
 //
-// Users: tests/golden/make_golden.py (golden vectors), tests/test_oracle.py (pins the C
-// restatement against the reference), bench.py (cpu_baseline and --impl reference).
+// Users: tests/golden/make_golden.py (golden vectors), tests/golden/make_trace_golden.py
+// (QKVTRACE file and recall_at_n fixtures), tests/test_oracle.py and tests/test_trace.py
+// (pin the C restatement and the trace/recall code against the reference), bench.py
+// (cpu_baseline and --impl reference).
 
 #include <chrono>
 #include <cstdint>
@@ -26,6 +28,7 @@
 #include "questkv/metrics.hpp"
 #include "questkv/parallel.hpp"
 #include "questkv/reference.hpp"
+#include "questkv/workloads.hpp"
 
 using namespace questkv;
 
@@ -229,4 +232,51 @@ int ref_layer_step(void* handle, const float* queries, uint32_t budget, int mode
     });
 }
 
+
+// QKVTRACE I/O through the reference (workloads.cpp write_trace / read_trace).
+int ref_write_trace(const char* path, uint32_t head_dim, uint32_t n, const float* keys,
+                    const float* values, const float* queries) {
+    return guarded([&] {
+        DecodeTrace t;
+        t.head_dim = head_dim;
+        t.steps.resize(n);
+        for (uint32_t i = 0; i < n; ++i) {
+            t.steps[i].key.assign(keys + size_t(i) * head_dim, keys + size_t(i + 1) * head_dim);
+            t.steps[i].value.assign(values + size_t(i) * head_dim, values + size_t(i + 1) * head_dim);
+            t.steps[i].query.assign(queries + size_t(i) * head_dim, queries + size_t(i + 1) * head_dim);
+        }
+        write_trace(path, t);
+    });
+}
+
+// read_trace: -> head_dim, length; copies up to cap steps. Status 4 = trace_format_error.
+int ref_read_trace(const char* path, uint32_t* head_dim, uint32_t* n, float* keys, float* values,
+                   float* queries, uint32_t cap) {
+    try {
+        const DecodeTrace t = read_trace(path);
+        *head_dim = t.head_dim;
+        *n = uint32_t(t.steps.size());
+        for (uint32_t i = 0; i < *n && i < cap; ++i) {
+            std::memcpy(keys + size_t(i) * t.head_dim, t.steps[i].key.data(), t.head_dim * 4);
+            std::memcpy(values + size_t(i) * t.head_dim, t.steps[i].value.data(), t.head_dim * 4);
+            std::memcpy(queries + size_t(i) * t.head_dim, t.steps[i].query.data(), t.head_dim * 4);
+        }
+        return 0;
+    } catch (const trace_format_error&) {
+        return 4;
+    } catch (...) {
+        return 3;
+    }
+}
+
+// recall_at_n (metrics.cpp:12-38) over a cache built from n_tokens appends.
+int ref_recall_at_n(const uint32_t* selected, uint32_t n_sel, const float* query, const float* keys,
+                    const float* values, uint32_t n_tokens, uint32_t dim, uint32_t page_size,
+                    uint32_t top_n, double* recall) {
+    return guarded([&] {
+        KvCache cache = make_cache(keys, values, n_tokens, dim, page_size);
+        *recall = recall_at_n(std::span<const uint32_t>(selected, n_sel),
+                              std::span<const float>(query, dim), cache, top_n);
+    });
+}
 }  // extern "C"
