@@ -93,6 +93,8 @@ class Layer:
     (1, 4, 4, 128, [32800], 2048),        # 2051 pages: per-CTA tail pass, 256-thread select
     (1, 4, 4, 128, [65000], 2048),        # 4063 pages: two estimate passes per CTA
     (1, 2, 2, 128, [70000], 2048),        # 4375 pages: the 512-thread select
+    (1, 80, 80, 64, [9300], 1024),        # cluster 1, 582 pages per CTA: pipelined passes, d=64
+    (1, 40, 40, 128, [19000], 2048),      # cluster 2, 594 pages per CTA: pipelined passes
 ])
 @pytest.mark.parametrize("keep", [True, False])
 def test_fused_step_vs_oracle(qk, oracle_c, B, Hq, Hkv, d, lens, budget, keep):
