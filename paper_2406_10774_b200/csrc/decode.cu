@@ -377,7 +377,9 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
     const uint32_t n_cand = all_pages ? 0u : (p.force ? P - 1 : P);
     const uint32_t n_est = p.keep_scores ? P : n_cand;
     const bool smem_keys = p.key_cap != 0 && key_slots(n_cand) <= p.key_cap;
-    if (tid == 0 && smem_keys && n_cand > 0) mbar_expect_tx_only(keys_bar, uint32_t(G) * n_cand * 8u);
+    // (A one-CTA cluster exchanges nothing: plain shared stores and a CTA barrier.)
+    if (tid == 0 && smem_keys && n_cand > 0 && C > 1)
+        mbar_expect_tx_only(keys_bar, uint32_t(G) * n_cand * 8u);
     // This CTA's estimate range: contiguous, a multiple of 8 pages (16-byte metadata
     // pieces), balanced over the cluster.
     const uint32_t per = ((n_est + C - 1) / C + 7) & ~7u;
@@ -518,7 +520,9 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
             if (smem_keys) {
                 if (pg < n_cand) {
                     const unsigned long long k = order_key(sc);
-                    for (uint32_t r = 0; r < C; ++r) st_async_u64(map_rank(keys + key_slot(pg), r), k, map_rank(keys_bar, r));
+                    if (C == 1) keys[key_slot(pg)] = k;
+                    else
+                        for (uint32_t r = 0; r < C; ++r) st_async_u64(map_rank(keys + key_slot(pg), r), k, map_rank(keys_bar, r));
                 }
             }
             if (!smem_keys || p.keep_scores)
@@ -541,7 +545,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
             // The append overlaps the loads above (s_new_* are read after the barrier below).
             if (owner && !appended) {
                 do_append();
-                if (smem_keys) arrive_keys(true);  // the new K/V row released early
+                if (smem_keys && C > 1) arrive_keys(true);  // the new K/V row released early
             }
             if (tail && c0 == r_begin) {
                 // The staged tail pages (issued first) are finished while this pass's
@@ -720,7 +724,9 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
                             // Push the key to every CTA of the cluster (padded slot).
                             const unsigned long long k = order_key(sc);
                             unsigned long long* dst = keys + size_t(g) * p.key_cap + key_slot(pg);
-                            for (uint32_t r = 0; r < C; ++r) st_async_u64(map_rank(dst, r), k, map_rank(keys_bar, r));
+                            if (C == 1) *dst = k;
+                            else
+                                for (uint32_t r = 0; r < C; ++r) st_async_u64(map_rank(dst, r), k, map_rank(keys_bar, r));
                         }
                     }
                     if (!smem_keys || p.keep_scores)
@@ -736,8 +742,12 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
     // Keys of every CTA of the unit are visible after this barrier (and so is the new K/V
     // row written in phase A).
     stamp(p.probe, 8);
-    if (!arrived) arrive_keys(!smem_keys || owner);
-    mbar_wait_cluster(keys_bar, 0);
+    if (C > 1) {
+        if (!arrived) arrive_keys(!smem_keys || owner);
+        mbar_wait_cluster(keys_bar, 0);
+    } else {
+        __syncthreads();  // this CTA's keys (or HBM scores) and its appended row
+    }
     stamp(p.probe, 9);
     if (append && rank == 0 && tid == kThreads - 1) {  // off the selection warps' path
         // Every CTA of this unit has read the old length.  The last unit of the sequence
