@@ -249,3 +249,38 @@ def test_fused_graph_replay_outgrows_capture(qk, oracle_c):
         _, _, o_want = oracle_c.quest_step(qs[-1][0, h], eager.keys[0][h], eager.vals[0][h], S,
                                            2048, True, True)
         assert rel_l2(out[0, h], o_want) <= TOL, h
+
+
+@pytest.mark.parametrize("Hq,Hkv,L,budget", [
+    (4, 4, 8000, 1024),     # 500 pages: 128-thread group
+    (4, 4, 32800, 2048),    # 2051 pages: 256-thread group
+    (2, 2, 70000, 4096),    # 4375 pages: the 512-thread select
+    (8, 2, 6000, 512),      # GQA 4: per-head groups
+])
+def test_fused_selection_heavy_ties(qk, oracle_c, Hq, Hkv, L, budget):
+    """Keys and queries from tiny value sets: most pages share a score, the boundary bin
+    holds far more than 32 keys and the fused kernel takes its multi-pass 64-bit selection
+    (ties to the lower page, as criticality.cpp:64-67).  Pages bitwise, outputs 1e-5."""
+    rng = np.random.default_rng(L + Hq)
+    d, S = 128, 16
+    vals = np.array([-0.25, 0.0, 0.25], np.float32)
+    layer = Layer(qk, rng, 1, Hq, Hkv, d, S, [1], extra=L + 16)
+    keys = rng.choice(vals, size=(Hkv, L - 1, d)).astype(np.float32)
+    keys[:, :, 4:] = 0.0  # only 4 channels vary: few distinct page bounds
+    values = half(rng.standard_normal((Hkv, L - 1, d)) * 0.1)
+    layer.qc = qk.QuestCache(d, S, max_batch=1, num_q_heads=Hq, num_kv_heads=Hkv, max_tokens=L + 16)
+    layer.qc.keep_step_scores(True)
+    layer.qc.prefill(0, 0, torch.from_numpy(keys).half().cuda(), torch.from_numpy(values).half().cuda())
+    layer.keys, layer.vals = [keys], [values]
+    q = half(rng.choice(np.array([-1.0, 1.0], np.float32), size=(1, Hq, d)))
+    kn = half(rng.choice(vals, size=(1, Hkv, d)))
+    vn = half(rng.standard_normal((1, Hkv, d)) * 0.1)
+    layer.keys[0] = np.concatenate([layer.keys[0], kn[0][:, None]], axis=1)
+    layer.vals[0] = np.concatenate([layer.vals[0], vn[0][:, None]], axis=1)
+    P = L // S + 1
+    pages = torch.full((1, Hq, P), -1, dtype=torch.int32, device="cuda")
+    counts = torch.zeros((1, Hq), dtype=torch.int32, device="cuda")
+    t = lambda a: torch.from_numpy(a).half().cuda()  # noqa: E731
+    out = layer.qc.decode_step(0, t(q), t(kn), t(vn), budget, pages=pages, counts=counts)
+    layer.qc.check_status()
+    layer.check(oracle_c, q, out.cpu().numpy(), pages.cpu().numpy(), counts.cpu().numpy(), budget)
