@@ -83,10 +83,6 @@ __device__ __forceinline__ uint32_t cluster_size() {
     asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
     return r;
 }
-__device__ __forceinline__ void cluster_sync_acqrel() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n"
-                 "barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-}
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -94,13 +90,6 @@ __device__ __forceinline__ uint32_t map_rank(const void* local_addr, uint32_t ra
     uint32_t ra;
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(local_addr)), "r"(rank));
     return ra;
-}
-__device__ __forceinline__ void st_cluster_f32(float* local_addr, uint32_t rank, float v) {
-    asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(map_rank(local_addr, rank)), "f"(v)
-                 : "memory");
-}
-__device__ __forceinline__ void st_cluster_u64(uint32_t cluster_addr, unsigned long long v) {
-    asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(cluster_addr), "l"(v) : "memory");
 }
 
 // Asynchronous remote shared-memory stores that complete transaction bytes on the
@@ -127,9 +116,6 @@ __device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, uint32_t
 __device__ __forceinline__ void mbar_expect_tx_only(unsigned long long* bar, uint32_t bytes) {
     asm volatile("mbarrier.expect_tx.relaxed.cluster.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)),
                  "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_remote_release(uint32_t cluster_bar) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
     asm volatile(
