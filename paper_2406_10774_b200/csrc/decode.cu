@@ -556,14 +556,16 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
             double acc[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+            if (__any_sync(0xffffffffu, act)) {  // short ranges leave whole warps without pages
 #pragma unroll
-            for (int k = 0; k < CPG; ++k) {
-                const int c = cg * CPG + k;
-                const double w = dq[c];
-                const unsigned short* h = reinterpret_cast<const unsigned short*>(&v[k]);
+                for (int k = 0; k < CPG; ++k) {
+                    const int c = cg * CPG + k;
+                    const double w = dq[c];
+                    const unsigned short* h = reinterpret_cast<const unsigned short*>(&v[k]);
 #pragma unroll
-                for (int j = 0; j < 8; ++j)
-                    acc[j] = __fma_rn(w, (c & 1) ? h2d_scaled(h[j]) : h2d(__ushort_as_half(h[j])), acc[j]);
+                    for (int j = 0; j < 8; ++j)
+                        acc[j] = __fma_rn(w, (c & 1) ? h2d_scaled(h[j]) : h2d(__ushort_as_half(h[j])), acc[j]);
+                }
             }
             if (c0 == r_begin) stamp(p.probe, 5);
             double2* dst = reinterpret_cast<double2*>(part + cg * kThreads + half * 256 + lane * 8);
