@@ -50,6 +50,14 @@ __global__ void __launch_bounds__(512, 1) attend(const __half* __restrict__ kpoo
             const int pg = pl[i];
             warp_fold_page<D, false>(ks + size_t(pg) * S * D, vs + size_t(pg) * S * D, S, qf, 0.1f, m, l, o);
         }
+    } else if (MODE == 3) {
+        // MODE 3: the warp's two pages interleaved by halves: the first halves of both pages
+        // in flight together (same registers as one full page), then the second halves.
+        const int pa = pl[warp], pb = pl[warp + 16];
+        for (int hh = 0; hh < 2; ++hh) {
+            warp_fold_page<D, true>(ks + size_t(pa) * S * D + hh * 8 * D, vs + size_t(pa) * S * D + hh * 8 * D, 8, qf, 0.1f, m, l, o);
+            warp_fold_page<D, true>(ks + size_t(pb) * S * D + hh * 8 * D, vs + size_t(pb) * S * D + hh * 8 * D, 8, qf, 0.1f, m, l, o);
+        }
     } else {
         // MODE 2: half a page per warp-iteration, four iterations (more, smaller batches).
         for (int i = warp; i < 64; i += 16) {
@@ -119,6 +127,7 @@ int main() {
             if (mode == 0) attend<0><<<ctas, 512>>>(k + off, v + off, slice, pages, q, out, ts);
             if (mode == 1) attend<1><<<ctas, 512>>>(k + off, v + off, slice, pages, q, out, ts);
             if (mode == 2) attend<2><<<ctas, 512>>>(k + off, v + off, slice, pages, q, out, ts);
+            if (mode == 3) attend<3><<<ctas, 512>>>(k + off, v + off, slice, pages, q, out, ts);
             cudaDeviceSynchronize();
             cudaMemcpy(h.data(), ts, ctas * 16, cudaMemcpyDeviceToHost);
             std::vector<double> d(ctas);
@@ -136,7 +145,7 @@ int main() {
         }
         printf("mode %d %s: per-CTA median %.2f us, span %.2f us\n", mode, cold ? "cold" : "warm", best_med, best_max);
     };
-    for (int mode = 0; mode < 3; ++mode) {
+    for (int mode = 0; mode < 4; ++mode) {
         run(mode, false);
         run(mode, true);
     }
