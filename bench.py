@@ -12,9 +12,15 @@ captured once in a CUDA graph.  `value` is microseconds per layer (step time / N
 32 layer caches are 17 GB, so every layer's 67 MB working set comes from HBM, not L2
 (each layer is revisited only after 31 other layers have streamed ~2 GB through L2).
 
-N > 1 (torchrun): each rank serves its own request (weak scaling, no collective on the
-attention path); the step time is the max over ranks and `value` is the whole job's time
-per layer-step: max_time / (NL * N).
+N > 1 (`--gpus N`; bench.py re-launches itself under torch.distributed.run when WORLD_SIZE
+is unset, and refuses a WORLD_SIZE that differs from N):
+  --shard requests (default, weak scaling): each rank serves its own batch of requests, no
+      collective on the attention path; `value` = max_time / (NL * N), the whole job's time
+      per request-layer.
+  --shard heads (strong scaling): the config's (request, KV head) units are
+      partitioned over the ranks (shard.partition; GQA groups stay on one GPU) and the
+      per-head outputs are all-gathered over NCCL inside the e2e timed region; `value` =
+      max_time / NL.  Per-GPU kernel time is reported separately (per_gpu_us_per_layer).
 
 --impl reference: the reference's own CPU implementation (oracle/_ref, compiled from
 /root/reference) of the same path on the host cores: estimate_all -> select_top_k ->
@@ -64,6 +70,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="cfg2")
+    ap.add_argument("--shard", choices=["requests", "heads"], default="requests")
     ap.add_argument("--ctx", type=int, default=None)
     ap.add_argument("--budget", type=int, default=None)
     ap.add_argument("--layers", type=int, default=None)
@@ -80,21 +87,97 @@ def dist_env():
     return rank, world, local
 
 
-def algorithmic_bytes(lengths, heads, head_dim, page, budget, bpe=2):
-    """Reference byte accounting (metrics.cpp:90-108) for one layer step: per head,
-    metadata 2*d*bpe per page + K/V 2*d*bpe per attended token (the selected pages'
-    actual lengths; force-recent keeps the possibly partial newest page)."""
+def relaunch_if_needed(args):
+    """--gpus N without a torchrun environment: run N ranks of this script under
+    torch.distributed.run (one process per GPU) and exit with its status."""
+    world = os.environ.get("WORLD_SIZE")
+    if world is not None:
+        if int(world) != args.gpus:
+            sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+        return
+    if args.gpus <= 1:
+        return
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
+class Workload:
+    """The benchmarked configuration (shared by both arms, so their `config` dicts match)."""
+
+    def __init__(self, args, world):
+        HQ, HKV, ctx0, budget0, B, NL0, desc = CONFIGS[args.config]
+        self.name, self.HQ, self.HKV, self.B, self.desc = args.config, HQ, HKV, B, desc
+        self.ctx = args.ctx if args.ctx else ctx0
+        self.budget = args.budget if args.budget else budget0
+        self.NL = args.layers if args.layers else NL0
+        self.world, self.shard = world, args.shard
+        if args.shard == "heads":
+            self.global_batch = B
+            par = f"(request, KV head) units partitioned over {world} GPU(s), NCCL output gather"
+            scaling = "strong"
+        else:
+            self.global_batch = B * world
+            par = f"request-sharded x{world} (no collective)"
+            scaling = "weak"
+        self.scaling = scaling
+        self.config = {
+            "workload": desc + "; one step = one decode step (append + estimate + top-K + "
+                        f"sparse attend) through {self.NL} independent layer caches",
+            "name": self.name, "seq_len": self.ctx, "budget": self.budget, "q_heads": HQ,
+            "kv_heads": HKV, "head_dim": HEAD_DIM, "page_size": PAGE,
+            "layers_per_step": self.NL, "batch_per_gpu": B if args.shard == "requests" else None,
+            "global_batch": self.global_batch, "parallelism": par,
+            "l2": f"inputs larger than L2: {self.NL} rotating layer caches, each revisited after "
+                  f"{self.NL - 1} other layers' traffic",
+        }
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def page_lengths_tokens(L, page, pages):
+    """Tokens held by `pages` (sorted page indices) of an L-token cache."""
+    P = (L + page - 1) // page
+    last = L - (P - 1) * page
+    return sum(last if p == P - 1 else page for p in pages)
+
+
+def algorithmic_bytes(lengths, heads, head_dim, page, budget, bpe=2, kv_heads=None,
+                      union_tokens=None):
+    """Reference byte accounting (metrics.cpp:90-108) for one layer step.
+    Per (request, KV head): metadata 2*d*bpe per page + K/V 2*d*bpe per token of the UNION
+    of the pages its query heads selected.  MHA: the union is the head's own selection,
+    top-(K-1) full pages + the (possibly partial) newest page.  GQA: pass the measured
+    union size per (request, KV head) in `union_tokens` (tokens)."""
+    kv_heads = heads if kv_heads is None else kv_heads
     total = 0
     vec = head_dim * bpe
     for L in lengths:
         P = (L + page - 1) // page
         k = budget // page
         last_len = L - (P - 1) * page
-        if k >= P:
+        if union_tokens is not None:
+            attended = union_tokens
+        elif k >= P:
             attended = L
         else:
             attended = (k - 1) * page + last_len  # top-(K-1) full pages + the newest page
-        total += heads * (2 * vec * P + 2 * vec * attended)
+        total += kv_heads * (2 * vec * P + 2 * vec * attended)
     return total
 
 
@@ -186,10 +269,7 @@ def profiled_traffic():
     return None
 
 
-def cpu_baseline_sample(ctx, budget, threads, reps=2):
-    """The reference (oracle/_ref) on one full layer: 32 heads at `ctx` tokens."""
-    from oracle import REF_SO, Oracle, Reference  # checker / baseline only
-
+def synthetic_layer(ctx):
     rng = np.random.default_rng(1)
     sd = 1.0 / np.sqrt(HEAD_DIM)
     keys = (rng.standard_normal((HEADS, ctx, HEAD_DIM), dtype=np.float32) * sd)
@@ -197,26 +277,40 @@ def cpu_baseline_sample(ctx, budget, threads, reps=2):
     vals = (rng.standard_normal((HEADS, ctx, HEAD_DIM), dtype=np.float32) * sd)
     vals = vals.astype(np.float16).astype(np.float32)
     q = (rng.standard_normal((HEADS, HEAD_DIM)) * sd).astype(np.float16).astype(np.float32)
+    return keys, vals, q
+
+
+def cpu_baseline_sample(ctx, budget, threads, warmup=3, reps=10):
+    """The reference (oracle/_ref) on one full layer, 32 heads at `ctx` tokens, phases as
+    cmd_bench (warmup 3, reps 10, cmd_bench.cpp:32-51), on all host threads and on one."""
+    from oracle import REF_SO, Oracle, Reference  # checker / baseline only
+
+    keys, vals, q = synthetic_layer(ctx)
+    sample = (f"1 layer = {HEADS} heads x {ctx} tokens, d={HEAD_DIM}, S={PAGE}, budget {budget}; "
+              "estimate_all->select_top_k->sparse_attention per head via questkv::parallel_for")
     if os.path.exists(REF_SO):
-        ref = Reference()
-        layer = ref.layer(keys, vals, PAGE)
-        mean_ns, min_ns, _ = layer.step(q, budget, threads=threads, warmup=1, reps=reps)
+        layer = Reference().layer(keys, vals, PAGE)
+        mean_ns, min_ns, _ = layer.step(q, budget, threads=threads, warmup=warmup, reps=reps)
+        mean1, min1, _ = layer.step(q, budget, threads=1, warmup=1, reps=3)
         layer.close()
-        kind = "reference"
-    else:  # the C restatement, one head at a time (single thread)
-        orc = Oracle()
-        t0 = time.perf_counter()
-        for h in range(HEADS):
-            orc.quest_step(q[h], keys[h], vals[h], PAGE, budget)
-        mean_ns = (time.perf_counter() - t0) * 1e9
-        kind, threads = "port", 1
-    return {"value": mean_ns / 1e3, "unit": UNIT, "cores": threads, "kind": kind,
-            "sample": f"1 layer = {HEADS} heads x {ctx} tokens, d={HEAD_DIM}, S={PAGE}, "
-                      f"budget {budget}; estimate_all->select_top_k->sparse_attention per head "
-                      f"via questkv::parallel_for; mean of {reps} reps after 1 warmup"}
+        return {"value": round(mean_ns / 1e3, 3), "unit": UNIT, "cores": threads,
+                "kind": "reference", "min": round(min_ns / 1e3, 3),
+                "one_thread": {"value": round(mean1 / 1e3, 3), "min": round(min1 / 1e3, 3),
+                               "reps": 3},
+                "cpu": cpu_model(),
+                "sample": sample + f"; mean of {reps} reps after {warmup} warmup"}
+    orc = Oracle()  # the C restatement, one head at a time (single thread)
+    t0 = time.perf_counter()
+    for h in range(HEADS):
+        orc.quest_step(q[h], keys[h], vals[h], PAGE, budget)
+    us = (time.perf_counter() - t0) * 1e6
+    return {"value": round(us, 3), "unit": UNIT, "cores": 1, "kind": "port", "cpu": cpu_model(),
+            "sample": sample + "; one pass"}
 
 
 def run_reference(args):
+    """The reference's own CPU path (oracle/_ref = the unmodified reference compiled from
+    /root/reference) on the host cores: every step is one full layer of the workload."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
@@ -226,34 +320,25 @@ def run_reference(args):
     if not os.path.exists(REF_SO):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return
-    HQ, _, ctx0, budget0, _, _, desc = CONFIGS[args.config]
-    ctx = args.ctx if args.ctx else ctx0
-    budget = args.budget if args.budget else budget0
-    rng = np.random.default_rng(1)
-    sd = 1.0 / np.sqrt(HEAD_DIM)
-    keys = (rng.standard_normal((HEADS, ctx, HEAD_DIM), dtype=np.float32) * sd)
-    keys = keys.astype(np.float16).astype(np.float32)
-    vals = (rng.standard_normal((HEADS, ctx, HEAD_DIM), dtype=np.float32) * sd)
-    vals = vals.astype(np.float16).astype(np.float32)
-    q = (rng.standard_normal((HEADS, HEAD_DIM)) * sd).astype(np.float16).astype(np.float32)
+    w = Workload(args, world)
+    keys, vals, q = synthetic_layer(w.ctx)
     layer = Reference().layer(keys, vals, PAGE)
-    steps = max(1, min(args.steps, 20))
-    mean_ns, min_ns, _ = layer.step(q, budget, threads=threads, warmup=max(1, min(args.warmup, 3)),
-                                    reps=steps)
+    steps, warmup = max(1, args.steps), max(0, args.warmup)
+    mean_ns, min_ns, _ = layer.step(q, w.budget, threads=threads, warmup=warmup, reps=steps)
     layer.close()
     us = mean_ns / 1e3
     line = {
         "metric": METRIC, "value": round(us, 3), "unit": UNIT, "impl": "reference",
-        "n_gpus": args.gpus, "steps": steps, "warmup": max(1, min(args.warmup, 3)),
-        "ms_per_step": round(mean_ns / 1e6, 4), "higher_is_better": False, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic N(0,1/d) fp16-representable",
-        "config": {"workload": desc + "; one layer (one sequence, 32 heads) per step on the host "
-                               "CPU",
-                   "name": args.config,
-                   "seq_len": ctx, "budget": budget, "heads": HEADS},
+        "n_gpus": args.gpus, "steps": steps, "warmup": warmup,
+        "ms_per_step": round(mean_ns * w.NL / 1e6, 4), "higher_is_better": False,
+        "scaling": w.scaling, "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic N(0,1/d) fp16-representable",
+        "config": w.config,
         "cpu_baseline": {"value": round(us, 3), "unit": UNIT, "cores": threads,
-                         "kind": "reference",
-                         "sample": f"every step = 1 full layer ({HEADS} heads x {ctx} tokens)"},
+                         "kind": "reference", "cpu": cpu_model(),
+                         "sample": f"every step = 1 full layer ({HEADS} heads x {w.ctx} tokens, "
+                                   f"budget {w.budget}) on the host; ms_per_step = "
+                                   f"{w.NL} layers x the per-layer mean"},
         "e2e": {"value": round(us, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "min_us_per_layer": round(min_ns / 1e3, 3),
@@ -261,13 +346,12 @@ def run_reference(args):
     print(json.dumps(line))
 
 
-
-
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
     from paper_2406_10774_b200 import QuestCache
+    from paper_2406_10774_b200.shard import gather_outputs, partition
 
     rank, world, local = dist_env()
     if world > 1:
@@ -275,39 +359,44 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    HQ, HKV, ctx0, budget0, B, NL0, desc = CONFIGS[args.config]
-    ctx = args.ctx if args.ctx else ctx0
-    budget = args.budget if args.budget else budget0
-    NL = args.layers if args.layers else NL0
+    w = Workload(args, world)
+    HQ, HKV, B, NL, ctx, budget = w.HQ, w.HKV, w.B, w.NL, w.ctx, w.budget
+    G = HQ // HKV
+    shards = partition(B, HKV, world) if args.shard == "heads" else None
+    if shards is not None:
+        lb, lkv = shards[rank].num_requests, shards[rank].num_kv_heads
+    else:
+        lb, lkv = B, HKV
+    lq = lkv * G
     headroom = args.warmup + args.steps + args.e2e_steps + 8
-    qc = QuestCache(HEAD_DIM, PAGE, num_layers=NL, max_batch=B, num_q_heads=HQ,
-                    num_kv_heads=HKV, max_tokens=ctx + headroom, device=local)
+    qc = QuestCache(HEAD_DIM, PAGE, num_layers=NL, max_batch=lb, num_q_heads=lq,
+                    num_kv_heads=lkv, max_tokens=ctx + headroom, device=local)
     g = torch.Generator(device=dev)
     g.manual_seed(1234 + rank)
     sd = 1.0 / HEAD_DIM ** 0.5
     n0 = ctx - 1  # the first timed step appends token ctx-1 -> a full `ctx` context
     for layer in range(NL):
-        for bb in range(B):
-            k = (torch.randn((HKV, n0, HEAD_DIM), generator=g, device=dev) * sd).half()
-            v = (torch.randn((HKV, n0, HEAD_DIM), generator=g, device=dev) * sd).half()
+        for bb in range(lb):
+            k = (torch.randn((lkv, n0, HEAD_DIM), generator=g, device=dev) * sd).half()
+            v = (torch.randn((lkv, n0, HEAD_DIM), generator=g, device=dev) * sd).half()
             qc.prefill(layer, bb, k, v)
             del k, v
     total_steps = args.warmup + args.steps
-    q = (torch.randn((total_steps, NL, B, HQ, HEAD_DIM), generator=g, device=dev) * sd).half()
-    kn = (torch.randn((total_steps, NL, B, HKV, HEAD_DIM), generator=g, device=dev) * sd).half()
-    vn = (torch.randn((total_steps, NL, B, HKV, HEAD_DIM), generator=g, device=dev) * sd).half()
+    q = (torch.randn((total_steps, NL, lb, lq, HEAD_DIM), generator=g, device=dev) * sd).half()
+    kn = (torch.randn((total_steps, NL, lb, lkv, HEAD_DIM), generator=g, device=dev) * sd).half()
+    vn = (torch.randn((total_steps, NL, lb, lkv, HEAD_DIM), generator=g, device=dev) * sd).half()
     qbuf, kbuf, vbuf = q[0].clone(), kn[0].clone(), vn[0].clone()
-    out = torch.empty((NL, B, HQ, HEAD_DIM), dtype=torch.float32, device=dev)
+    out = torch.empty((NL, lb, lq, HEAD_DIM), dtype=torch.float32, device=dev)
     torch.cuda.synchronize()
 
     stream = torch.cuda.Stream(device=dev)
     # Load every kernel of the step eagerly on a throwaway cache of the same geometry
     # (lazy module loading must not happen inside the capture).
-    warm = QuestCache(HEAD_DIM, PAGE, num_layers=1, max_batch=B, num_q_heads=HQ,
-                      num_kv_heads=HKV, max_tokens=ctx + headroom, device=local)
-    for bb in range(B):
-        warm.prefill(0, bb, kn[0, 0, bb].view(HKV, 1, HEAD_DIM).contiguous(),
-                     vn[0, 0, bb].view(HKV, 1, HEAD_DIM).contiguous())
+    warm = QuestCache(HEAD_DIM, PAGE, num_layers=1, max_batch=lb, num_q_heads=lq,
+                      num_kv_heads=lkv, max_tokens=ctx + headroom, device=local)
+    for bb in range(lb):
+        warm.prefill(0, bb, kn[0, 0, bb].view(lkv, 1, HEAD_DIM).contiguous(),
+                     vn[0, 0, bb].view(lkv, 1, HEAD_DIM).contiguous())
     warm.decode_step(0, qbuf[0], kbuf[0], vbuf[0], budget, stream=stream)
     stream.synchronize()
     warm.close()
@@ -344,7 +433,8 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    elapsed_ms = ev0.elapsed_time(ev1)
+    own_ms = ev0.elapsed_time(ev1)
+    elapsed_ms = own_ms
     qc.sync_lengths(stream=stream)  # graph replays advanced only the device lengths
     qc.check_status(stream=stream)
     if world > 1:
@@ -353,47 +443,105 @@ def run_ours(args):
         elapsed_ms = float(t.item())
     ms_per_step = elapsed_ms / args.steps
     us_per_layer = ms_per_step * 1e3 / NL
-    value = us_per_layer / world
+    value = us_per_layer / world if args.shard == "requests" else us_per_layer
 
-    # Algorithmic bytes of the timed steps (reference accounting per query head, every
-    # sequence of the batch).
+    # Algorithmic bytes of the timed steps on this GPU (reference accounting).
+    # GQA: the K/V term counts the union of the pages a KV head's query heads selected,
+    # measured on the final state (one extra, untimed, non-appending step per layer).
+    union = None
+    if G > 1:
+        pages = torch.full((lb, lq, max(1, budget // PAGE)), -1, dtype=torch.int32, device=dev)
+        counts = torch.zeros((lb, lq), dtype=torch.int32, device=dev)
+        L_now = qc.token_count(0, 0)
+        tot, n = 0, 0
+        scratch = torch.empty((lb, lq, HEAD_DIM), dtype=torch.float32, device=dev)
+        for layer in range(NL):
+            qc.decode_step(layer, q[total_steps - 1, layer], None, None, budget, out=scratch,
+                           pages=pages, counts=counts, stream=stream)
+            stream.synchronize()
+            pc, cc = pages.cpu().numpy(), counts.cpu().numpy()
+            for bb in range(lb):
+                for h in range(lkv):
+                    sel = set()
+                    for gq in range(G):
+                        sel.update(pc[bb, h * G + gq, :cc[bb, h * G + gq]].tolist())
+                    tot += page_lengths_tokens(L_now, PAGE, sorted(sel))
+                    n += 1
+        union = tot / max(n, 1)
     bytes_total = 0
     for i in range(args.warmup, total_steps):
         L = ctx + i  # tokens after this step's append (first replay -> ctx)
-        bytes_total += B * algorithmic_bytes([L], HQ, HEAD_DIM, PAGE, budget)
+        bytes_total += lb * algorithmic_bytes([L], lq, HEAD_DIM, PAGE, budget, kv_heads=lkv,
+                                              union_tokens=union)
     bytes_per_layer = bytes_total / args.steps
+    own_us_per_layer = own_ms * 1e3 / (args.steps * NL)
     achieved_gbs = bytes_per_layer / (us_per_layer * 1e-6) / 1e9
     peak, peak_src = measured_peaks()
+    traffic = profiled_traffic() if args.config == "cfg2" and world == 1 else None
 
     # Per-kernel breakdown (one layer, eager, CUDA events) on the current state.
-    breakdown = kernel_breakdown(qc, q[0], NL, budget, stream) if rank == 0 and B == 1 else {}
+    breakdown = kernel_breakdown(qc, q[0], NL, budget, stream) if rank == 0 and lb == 1 else {}
 
-    # End to end with host buffers: H2D of q/k/v and D2H of the fp32 output inside the
-    # timed region (qk_decode_step_host: the kernel reads/writes pinned mapped staging).
-    qh = torch.empty((NL, B, HQ, HEAD_DIM), dtype=torch.float16).pin_memory()
-    kh = torch.empty((NL, B, HKV, HEAD_DIM), dtype=torch.float16).pin_memory()
+    # End to end through the public API with host buffers: H2D of q/k/v and D2H of the
+    # fp32 output inside the timed region.
+    qh = torch.empty((NL, lb, lq, HEAD_DIM), dtype=torch.float16).pin_memory()
+    kh = torch.empty((NL, lb, lkv, HEAD_DIM), dtype=torch.float16).pin_memory()
     vh = torch.empty_like(kh).pin_memory()
     qh.copy_(q[0].cpu())
     kh.copy_(kn[0].cpu())
     vh.copy_(vn[0].cpu())
-    oh = torch.empty((NL, B, HQ, HEAD_DIM), dtype=torch.float32).pin_memory()
-    qn, kn_, vn_, on = qh.numpy(), kh.numpy(), vh.numpy(), oh.numpy()
     e2e_steps = max(1, args.e2e_steps)
-    qc.decode_step_host(0, qn[0], kn_[0], vn_[0], budget, out=on[0], stream=stream)  # warm
-    if world > 1:
-        dist.barrier()
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        for layer in range(NL):
-            qc.decode_step_host(layer, qn[layer], kn_[layer], vn_[layer], budget, out=on[layer],
-                                stream=stream)
-    e2e_s = time.perf_counter() - t0
+    if shards is None:
+        # qk_decode_step_host: the kernel reads/writes pinned, mapped staging directly.
+        oh = torch.empty((NL, lb, lq, HEAD_DIM), dtype=torch.float32).pin_memory()
+        qn, kn_, vn_, on = qh.numpy(), kh.numpy(), vh.numpy(), oh.numpy()
+        qc.decode_step_host(0, qn[0], kn_[0], vn_[0], budget, out=on[0], stream=stream)  # warm
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            for layer in range(NL):
+                qc.decode_step_host(layer, qn[layer], kn_[layer], vn_[layer], budget,
+                                    out=on[layer], stream=stream)
+        e2e_s = time.perf_counter() - t0
+        e2e_path = "Python QuestCache.decode_step_host -> qk_decode_step_host (C ABI) per layer"
+        d2h = lq * lb * HEAD_DIM * 4 * NL
+    else:
+        # Sharded: H2D of this rank's q/k/v, the decode step, NCCL all-gather of every
+        # rank's per-head outputs, D2H of the full output -- per layer.
+        oh = torch.empty((NL, B, HQ, HEAD_DIM), dtype=torch.float32).pin_memory()
+        dq, dk, dv = torch.empty_like(qbuf[0]), torch.empty_like(kbuf[0]), torch.empty_like(vbuf[0])
+        lout = torch.empty((lb, lq, HEAD_DIM), dtype=torch.float32, device=dev)
+
+        def e2e_layer(layer):
+            with torch.cuda.stream(stream):  # the collective is ordered on `stream` too
+                dq.copy_(qh[layer], non_blocking=True)
+                dk.copy_(kh[layer], non_blocking=True)
+                dv.copy_(vh[layer], non_blocking=True)
+                qc.decode_step(layer, dq, dk, dv, budget, out=lout, stream=stream)
+                full = gather_outputs(lout, shards, B, HKV, G) if world > 1 else lout
+                oh[layer].copy_(full, non_blocking=True)
+            stream.synchronize()
+
+        torch.cuda.synchronize()
+        e2e_layer(0)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            for layer in range(NL):
+                e2e_layer(layer)
+        e2e_s = time.perf_counter() - t0
+        e2e_path = ("Python QuestCache.decode_step on this rank's units + NCCL all-gather of the "
+                    "per-head outputs (shard.gather_outputs) per layer")
+        d2h = HQ * B * HEAD_DIM * 4 * NL
     if world > 1:
         t = torch.tensor([e2e_s], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    e2e_us = e2e_s * 1e6 / (e2e_steps * NL) / world
-    e2e_path = "Python QuestCache.decode_step_host -> qk_decode_step_host (C ABI) per layer"
+    e2e_us = e2e_s * 1e6 / (e2e_steps * NL)
+    if args.shard == "requests":
+        e2e_us /= world
     # The native host API (C++ questkv_b200::DeviceCache::decode_step_host), compiled here
     # against the in-tree library; it replaces the Python number when it builds and runs.
     if world == 1 and not args.no_native_e2e and args.config == "cfg2":
@@ -402,9 +550,15 @@ def run_ours(args):
             e2e_us = native
             e2e_path = ("C++ questkv_b200::DeviceCache::decode_step_host (include/questkv_b200.hpp) "
                         "per layer, 8 layers x 20 steps; host q/k/v in, fp32 out to host")
-    h2d = (HQ + 2 * HKV) * B * HEAD_DIM * 2 * NL  # q, k, v fp16 per layer
-    d2h = HQ * B * HEAD_DIM * 4 * NL
+    h2d = (lq + 2 * lkv) * lb * HEAD_DIM * 2 * NL  # q, k, v fp16 per layer
 
+    per_gpu = torch.tensor([own_us_per_layer], device=dev)
+    if world > 1:
+        gathered = [torch.zeros_like(per_gpu) for _ in range(world)]
+        dist.all_gather(gathered, per_gpu)
+        per_gpu_list = [round(float(x.item()), 3) for x in gathered]
+    else:
+        per_gpu_list = [round(own_us_per_layer, 3)]
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -412,6 +566,11 @@ def run_ours(args):
     cpu = None
     if not args.no_cpu_baseline and world == 1 and args.config == "cfg2":
         cpu = cpu_baseline_sample(ctx, budget, os.cpu_count() or 1)
+    bytes_model = ("reference accounting metrics.cpp:90-108 / SURVEY §8d: per (request, KV head) "
+                   "2*d*2B per page of metadata + 2*d*2B per token of the union of its query "
+                   "heads' selected pages")
+    if union is not None:
+        bytes_model += f" (GQA union measured: {union:.1f} tokens per (request, KV head))"
     line = {
         "metric": METRIC,
         "value": round(value, 3),
@@ -421,32 +580,27 @@ def run_ours(args):
         "warmup": args.warmup,
         "ms_per_step": round(ms_per_step, 4),
         "higher_is_better": False,
-        "scaling": "weak",
+        "scaling": w.scaling,
         "vs_baseline": None,
         "dtype": "fp16 storage, fp64 estimate, fp32 attention accumulate",
         "data": "synthetic N(0,1/d) fp16 K/V/q (random-init, generated on device)",
-        "config": {
-            "workload": desc + "; step = append+estimate+top-K+sparse attend over "
-                        f"{NL} distinct layer caches (CUDA graph)",
-            "name": args.config, "seq_len": ctx, "budget": budget, "q_heads": HQ,
-            "kv_heads": HKV, "head_dim": HEAD_DIM, "page_size": PAGE, "layers_per_step": NL,
-            "batch_per_gpu": B, "global_batch": B * world,
-            "parallelism": f"request-sharded x{world} (no collective)",
-            "l2": f"inputs larger than L2: {NL} rotating layer caches, each revisited after "
-                  f"{NL - 1} other layers' traffic",
-        },
+        "config": w.config,
         "latency_us_per_layer": round(us_per_layer, 3),
-        "tokens_per_s": round(B * world * 1e6 / (us_per_layer * NL), 1),
+        "per_gpu_us_per_layer": per_gpu_list,
+        "tokens_per_s": round(w.global_batch * 1e6 / (us_per_layer * NL), 1),
         "achieved_hbm_gbs": round(achieved_gbs, 1),
         "roofline": {
             "bound": "hbm", "achieved": round(achieved_gbs, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved_gbs / peak, 4),
             "frac_at_8tbs": round(achieved_gbs / 8000.0, 4),  # report both fractions
-            "traffic": profiled_traffic() if args.config == "cfg2" else None,
+            "traffic": traffic,
+            "frac_physical": (round(traffic / (us_per_layer * 1e-6) / 1e9 / peak, 4)
+                              if traffic else None),
             "kernel": "decode_fused_kernel (one launch = append+estimate+top-K+attend of a layer)",
+            "timing": "per-layer time of the CUDA-graph replay (launch gaps included), CUDA "
+                      "events on the launching stream, max over ranks",
             "bytes_per_launch": int(bytes_per_layer),
-            "bytes_model": "reference accounting metrics.cpp:105-106: 2*d*2B per page (metadata) "
-                           "+ 2*d*2B per attended token, per query head",
+            "bytes_model": bytes_model,
             "peak_source": peak_src,
         },
         "kernel_breakdown_us": breakdown,
@@ -526,6 +680,7 @@ def kernel_breakdown(qc, q0, NL, budget, stream):
 
 def main():
     args = parse()
+    relaunch_if_needed(args)
     if args.impl == "reference":
         run_reference(args)
     else:

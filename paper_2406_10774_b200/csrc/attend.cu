@@ -56,6 +56,13 @@ attend_kernel(const __half* __restrict__ kp, const __half* __restrict__ vp,
     }
     const int pps = max(kMinPagesPerSplit, (count + kMaxSplits - 1) / kMaxSplits);
     const int nsplit = (count + pps - 1) / pps;
+    // A count past the list row, or needing more splits than the host launched, would read
+    // past the row or never complete the merge ticket: reject it (uniform over the CTAs of
+    // this (sequence, head), so no CTA takes the ticket).
+    if ((!dense && uint32_t(count) > pstride) || nsplit > int(gridDim.x)) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) record_status(status, QK_DEV_BAD_COUNT);
+        return;
+    }
     const int split = blockIdx.x;
     if (split >= nsplit) return;
     const int first = split * pps;

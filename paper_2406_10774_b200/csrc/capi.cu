@@ -5,8 +5,11 @@
 #include <cmath>
 #include <chrono>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <new>
 #include <string>
+#include <utility>
 
 #include "qk_internal.cuh"
 
@@ -24,6 +27,24 @@ int set_error(int code, const std::string& msg) {
 int cuda_check(cudaError_t err, const char* what) {
     if (err == cudaSuccess) return QK_OK;
     return set_error(QK_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(err));
+}
+
+int ensure_func_attrs(const void* func, size_t smem, int device, bool nonportable_cluster,
+                      const char* what) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, size_t> configured;  // (func, device) -> smem
+    std::lock_guard<std::mutex> lock(mu);
+    size_t& have = configured[{func, device}];
+    if (have >= smem && have != 0) return QK_OK;
+    if (int rc = cuda_check(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 int(smem)), what))
+        return rc;
+    if (nonportable_cluster)
+        if (int rc = cuda_check(cudaFuncSetAttribute(func, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
+                                what))
+            return rc;
+    have = smem ? smem : 1;
+    return QK_OK;
 }
 
 namespace {
@@ -491,8 +512,10 @@ int qk_decode_step_host(qk_cache* c, uint32_t layer, const uint16_t* q_host,
     // Inputs and output go through a pinned, device-mapped staging buffer that the fused
     // kernel reads and writes directly (zero-copy): one launch and one synchronisation per
     // call instead of three host-to-device copies, the kernel and a device-to-host copy.
-    const size_t in_max = size_t(c->B) * (c->Hq + 2 * c->Hkv) * hd * 2;
-    const size_t out_max = size_t(c->B) * c->Hq * hd * 4;
+    // Regions rounded to 64 bytes: the kernel does 4-byte output stores and the completion
+    // word is a 4-byte atomic (an odd head_dim would otherwise misalign both).
+    const size_t in_max = (size_t(c->B) * (c->Hq + 2 * c->Hkv) * hd * 2 + 63) & ~size_t(63);
+    const size_t out_max = (size_t(c->B) * c->Hq * hd * 4 + 63) & ~size_t(63);
     if (!c->host_stage) {
         void* h = nullptr;
         int rc = cuda_check(cudaHostAlloc(&h, in_max + out_max + 64, cudaHostAllocMapped), "cudaHostAlloc");
@@ -782,6 +805,9 @@ int qk_check_status(qk_cache* c, void* stream) {
             return set_error(QK_ERR_INVALID_ARGUMENT, "sparse_attention: empty page selection");
         case QK_DEV_CAPACITY:
             return set_error(QK_ERR_OUT_OF_RANGE, "KvCache::append: cache slice is full");
+        case QK_DEV_BAD_COUNT:
+            return set_error(QK_ERR_INVALID_ARGUMENT,
+                             "sparse_attention: page count exceeds the page list (pages_stride)");
         default: return set_error(QK_ERR_CUDA, "unknown device status");
     }
 }

@@ -362,7 +362,11 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
     const uint32_t count = all_pages ? P : p.k_budget;
     const uint32_t n_cand = all_pages ? 0u : (p.force ? P - 1 : P);
     const uint32_t n_est = p.keep_scores ? P : n_cand;
-    const bool smem_keys = p.key_cap != 0 && key_slots(n_cand) <= p.key_cap;
+    // Keys exchanged through the cluster's shared memory only when they fit the key array
+    // AND a shared-memory selection tier (phase C: <= kThreads*kSelKpt candidates);
+    // otherwise every CTA writes its scores to HBM and the selection reads them there.
+    const bool smem_keys = p.key_cap != 0 && key_slots(n_cand) <= p.key_cap &&
+                           n_cand <= uint32_t(kThreads * kSelKpt);
     // (A one-CTA cluster exchanges nothing: plain shared stores and a CTA barrier.)
     if (tid == 0 && smem_keys && n_cand > 0 && C > 1)
         mbar_expect_tx_only(keys_bar, uint32_t(G) * n_cand * 8u);
@@ -627,14 +631,15 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
 #pragma unroll 1
         for (int grp = 0; grp < kMetaGroups; ++grp) {
             cp_async_wait_n(kMetaGroups - 1 - grp);
-            if (patch && new_page >= c0 && new_page < c0 + PPC && tid < D &&
-                tid / CH_PER_GROUP == grp) {
-                // Replace the staged (pre-append) metadata of the newest page.
-                const int c = tid;
-                const uint32_t col = new_page - c0;
-                if (G == 1) {
-                    stage[size_t(c) * PPC + col] = (need[c] & 2) ? s_new_min[c] : s_new_max[c];
-                } else {
+            if (patch && new_page >= c0 && new_page < c0 + PPC) {  // CTA-uniform
+                // Replace the staged (pre-append) metadata of the newest page.  The column
+                // was copied by other threads' cp.async: every thread's copies of this
+                // group must have landed before the patch, or a late copy would overwrite
+                // it with the pre-append values.
+                __syncthreads();
+                if (tid < D && tid / CH_PER_GROUP == grp) {
+                    const int c = tid;
+                    const uint32_t col = new_page - c0;
                     stage[size_t(0 * D + c) * PPC + col] = s_new_min[c];
                     stage[size_t(1 * D + c) * PPC + col] = s_new_max[c];
                 }
@@ -998,15 +1003,9 @@ int run_fused(qk_cache* c, FusedParams prm, uint32_t batch, uint32_t cluster,
     }
     if (smem > kMaxSmem) return set_error(QK_ERR_UNSUPPORTED, "qk_decode_step: shared memory");
     auto kern = decode_fused_kernel<D, G>;
-    static size_t configured = 0;
-    if (smem > configured) {
-        int rc = cuda_check(
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
-            "decode_fused_kernel smem");
-        if (rc) return rc;
-        cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        configured = smem;
-    }
+    if (int rc = ensure_func_attrs(reinterpret_cast<const void*>(kern), smem, c->desc.device, true,
+                                   "decode_fused_kernel attributes"))
+        return rc;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(batch * c->Hkv * cluster);
     cfg.blockDim = dim3(kThreads);
@@ -1049,17 +1048,19 @@ int decode_unfused(qk_cache* c, uint32_t layer, const __half* q, const __half* k
     int rc = QK_OK;
     if (k) rc = launch_append(c, layer, k, v, batch, st);
     if (rc) return rc;
-    rc = launch_estimate(c, layer, q, batch, c->ws_scores, c->Pmax, max_pages, st);
+    // Grids and shared memory sized for the capacity, not this launch's pages: a CUDA graph
+    // captured now must stay correct when its replays grow the context.
+    rc = launch_estimate(c, layer, q, batch, c->ws_scores, c->Pmax, c->Pmax, st);
     if (rc) return rc;
     qk_selection_cfg eff = cfg;
     if (!cfg.per_layer_enabled) eff.token_budget = UINT32_MAX;
     int32_t* sel = pages ? pages : c->ws_pages;
     const uint32_t sstride = pages ? pstride : c->Pmax;
     int32_t* cnt = counts ? counts : c->ws_counts;
-    rc = launch_topk(c, layer, c->ws_scores, c->Pmax, batch, eff, sel, sstride, cnt, max_pages, st);
+    rc = launch_topk(c, layer, c->ws_scores, c->Pmax, batch, eff, sel, sstride, cnt, c->Pmax, st);
     if (rc) return rc;
     const uint32_t kk = eff.token_budget / c->S;
-    const uint32_t max_list = kk < max_pages ? kk : max_pages;
+    const uint32_t max_list = kk < c->Pmax ? kk : c->Pmax;
     return launch_attend(c, layer, q, batch, sel, sstride, cnt, false, max_list, out, out_dtype,
                          nullptr, st);
 }

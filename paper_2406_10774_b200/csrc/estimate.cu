@@ -173,11 +173,9 @@ int run(const qk_cache* c, uint32_t layer, const __half* q, uint32_t batch, doub
     const size_t smem = size_t(NROW) * D * PAGES * sizeof(__half) +
                         size_t(G == 1 ? 2 : G) * D * sizeof(double);
     auto kern = estimate_kernel<D, G, PAGES>;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        configured = true;
-    }
+    if (int rc = ensure_func_attrs(reinterpret_cast<const void*>(kern), smem, c->desc.device, false,
+                                   "estimate_kernel attributes"))
+        return rc;
     const uint32_t pages_per_cta = PAGES;
     const dim3 grid((max_pages + pages_per_cta - 1) / pages_per_cta, batch * c->Hkv);
     kern<<<grid, kThreads, smem, st>>>(c->meta, c->d_len, q, scores, layer, c->B, c->Hkv, c->S,

@@ -44,6 +44,11 @@ struct Status {
 
 int set_error(int code, const std::string& msg);
 int cuda_check(cudaError_t err, const char* what);
+// Kernel attributes are per device: raise `func`'s dynamic shared-memory limit to at least
+// `smem` bytes (and allow non-portable cluster sizes when asked) on `device`, once per
+// (function, device, size); thread-safe.
+int ensure_func_attrs(const void* func, size_t smem, int device, bool nonportable_cluster,
+                      const char* what);
 
 }  // namespace qk
 
@@ -97,6 +102,7 @@ enum : int32_t {
     QK_DEV_PAGE_NOT_ASCENDING = 2,
     QK_DEV_EMPTY_SELECTION = 3,
     QK_DEV_CAPACITY = 4,
+    QK_DEV_BAD_COUNT = 5,  // a page/token count past its list row or the launched splits
 };
 
 // Kernel launchers (one translation unit each).

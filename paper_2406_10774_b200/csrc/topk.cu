@@ -57,13 +57,14 @@ int launch_topk(const qk_cache* c, uint32_t layer, const double* scores, uint32_
                 uint32_t batch, const qk_selection_cfg& cfg, int32_t* pages,
                 uint32_t pstride, int32_t* counts, uint32_t max_pages, cudaStream_t st) {
     const uint32_t k = cfg.token_budget / c->S;
+    // Keys of up to max_pages pages per CTA; callers pass the cache capacity so that a CUDA
+    // graph captured now stays in bounds when replays grow the context.
+    if (max_pages < c->Pmax) max_pages = c->Pmax;
     const uint32_t kpt = (max_pages + kThreads - 1) / kThreads;
     const size_t smem = size_t(kThreads) * (kpt + 1) * sizeof(unsigned long long);
-    static size_t configured = 0;
-    if (smem > configured) {
-        cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        configured = smem;
-    }
+    if (int rc = ensure_func_attrs(reinterpret_cast<const void*>(topk_kernel), smem, c->desc.device,
+                                   false, "topk_kernel attributes"))
+        return rc;
     topk_kernel<<<batch * c->Hq, kThreads, smem, st>>>(scores, sstride, c->d_len, layer, c->B,
                                                        c->Hq, c->S, k, cfg.force_include_recent,
                                                        pages, pstride, counts);

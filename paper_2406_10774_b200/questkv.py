@@ -264,9 +264,29 @@ class QuestCache:
                          force_include_recent: bool = True, per_layer_enabled: bool = True,
                          out: Optional[np.ndarray] = None, stream=None) -> np.ndarray:
         """qk_decode_step_host: host fp16 arrays in, host fp32 output out (synchronous)."""
+        def host(a, shape, dtype, name):
+            if not isinstance(a, np.ndarray) or a.dtype != dtype:
+                raise ValueError(f"{name} must be a numpy {np.dtype(dtype).name} array")
+            if tuple(a.shape) != tuple(shape):
+                raise ValueError(f"{name} must have shape {tuple(shape)}, got {tuple(a.shape)}")
+            if not a.flags["C_CONTIGUOUS"]:
+                raise ValueError(f"{name} must be C-contiguous")
+            return a
+
+        if not isinstance(q, np.ndarray) or q.ndim != 3:
+            raise ValueError("q must be a numpy float16 array [batch, num_q_heads, head_dim]")
         batch = q.shape[0]
+        host(q, (batch, self.num_q_heads, self.head_dim), np.float16, "q")
+        if (k is None) != (v is None):
+            raise ValueError("k and v must both be given")
+        if k is not None:
+            host(k, (batch, self.num_kv_heads, self.head_dim), np.float16, "k")
+            host(v, (batch, self.num_kv_heads, self.head_dim), np.float16, "v")
         if out is None:
             out = np.empty((batch, self.num_q_heads, self.head_dim), dtype=np.float32)
+        host(out, (batch, self.num_q_heads, self.head_dim), np.float32, "out")
+        if not out.flags["WRITEABLE"]:
+            raise ValueError("out must be writeable")
         cfg = _sel_cfg(token_budget, force_include_recent, per_layer_enabled)
         check(self._lib.qk_decode_step_host(
             self._h, layer, q.ctypes.data, None if k is None else k.ctypes.data,
