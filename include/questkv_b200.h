@@ -33,6 +33,9 @@
  *   counts [batch][num_q_heads]                       int32
  *   out    [batch][num_q_heads][head_dim]             f32 or fp16 (qk_dtype)
  *   lse    [batch][num_q_heads]                       f32 natural-log LSE of logits/sqrt(d)
+ *   weights_sum [batch][num_q_heads]                  f64 AttentionOutput::weights_sum_check
+ *   tokens [batch][num_q_heads][tokens_stride]        int32, strictly ascending token indices
+ *   logits [batch][num_q_heads][logits_stride]        f64
  * Query head h reads KV head h / (num_q_heads / num_kv_heads) (GQA); every query head
  * selects its own pages (the reference's single-head semantics applied per query head).
  */
@@ -45,7 +48,7 @@
 extern "C" {
 #endif
 
-#define QK_ABI_VERSION 1
+#define QK_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define QK_API __attribute__((visibility("default")))
@@ -155,22 +158,68 @@ QK_API int qk_select_topk(const qk_cache *cache, uint32_t layer, const double *s
                    uint32_t scores_stride, uint32_t batch, const qk_selection_cfg *cfg,
                    int32_t *pages, uint32_t pages_stride, int32_t *counts, void *stream);
 
+/* select_top_k (criticality.cpp:36-81) on an ARBITRARY PageScore vector of one
+ * (layer, seq) cache: n (page_index, score) pairs in any order, repeated page indices
+ * allowed, exactly the reference's rule -- disabled -> every page; budget < page_size ->
+ * INVALID_ARGUMENT; n == 0 -> INVALID_ARGUMENT; a page_index >= page_count -> OUT_OF_RANGE
+ * (device status, qk_check_status); K >= n -> every page; else the first K by (score desc,
+ * page asc; -0 == +0), the K-th replaced by the newest page under force_include_recent,
+ * ascending (duplicates kept, as the reference).  pages holds pages_capacity entries
+ * (>= K, or >= page_count when every page is returned); *count = entries written.
+ * n <= 16384.  The fast form for estimate_all's output is qk_select_topk. */
+QK_API int qk_select_topk_pairs(qk_cache *cache, uint32_t layer, uint32_t seq,
+                         const uint32_t *page_index, const double *scores, uint32_t n,
+                         const qk_selection_cfg *cfg, int32_t *pages, uint32_t pages_capacity,
+                         int32_t *count, void *stream);
+
 /* sparse_attention (attention.cpp:94-116) over the listed pages, split-KV with an
  * fp32 log-sum-exp merge: logits q.k/sqrt(d), softmax renormalised over the selected
  * tokens, partial last page masked to its length.  Page lists must be strictly
  * ascending and in range (the form qk_select_topk writes); violations are recorded on
  * the device and reported by qk_check_status (the reference's out_of_range /
- * invalid_argument).  Every page count must be >= 1. */
+ * invalid_argument).  Every page count must be >= 1.  weights_sum (optional) receives
+ * AttentionOutput::weights_sum_check (attention.cpp:81): the post-softmax mass of the
+ * weights applied, evaluated in fp64 from the fp32 partials. */
 QK_API int qk_sparse_attend(const qk_cache *cache, uint32_t layer, const uint16_t *q,
                      uint32_t batch, const int32_t *pages, uint32_t pages_stride,
                      const int32_t *counts, void *out, int32_t out_dtype, float *lse,
-                     void *stream);
+                     double *weights_sum, void *stream);
 
 /* full_attention (attention.cpp:86-92): the same kernel over every page in order, so it
  * is bitwise equal to qk_sparse_attend given every page (the reference's full-budget
  * degeneracy, attention.hpp:34-36).  Empty sequence -> QK_ERR_INVALID_ARGUMENT. */
 QK_API int qk_dense_attend(const qk_cache *cache, uint32_t layer, const uint16_t *q,
-                    uint32_t batch, void *out, int32_t out_dtype, float *lse, void *stream);
+                    uint32_t batch, void *out, int32_t out_dtype, float *lse,
+                    double *weights_sum, void *stream);
+
+/* attend_tokens (attention.hpp:41-46, attention.cpp:69-84): attention over an explicit
+ * token set per (sequence, query head), the token-granular form policies use.  Lists are
+ * checked on the device like check_token_set (attention.cpp:19-30): an index >=
+ * token_count -> OUT_OF_RANGE, not strictly ascending -> INVALID_ARGUMENT, empty ->
+ * INVALID_ARGUMENT (reported by qk_check_status).  Chunks of page_size list entries are
+ * folded like pages, so every token in order is bitwise qk_dense_attend. */
+QK_API int qk_attend_tokens(const qk_cache *cache, uint32_t layer, const uint16_t *q,
+                     uint32_t batch, const int32_t *tokens, uint32_t tokens_stride,
+                     const int32_t *counts, void *out, int32_t out_dtype, float *lse,
+                     double *weights_sum, void *stream);
+
+/* attention_logits (attention.hpp:24-29, attention.cpp:34-52): logit_t = q.k_t / sqrt(d) in
+ * fp64, bitwise the reference's (exact fp16 products, sequential fp64 sum, correctly
+ * rounded sqrt and division).  tokens == NULL: every cached token of the sequence (the
+ * one-argument overload; logits_stride >= token_count); else the listed tokens, validated
+ * as qk_attend_tokens. */
+QK_API int qk_attention_logits(const qk_cache *cache, uint32_t layer, const uint16_t *q,
+                        uint32_t batch, const int32_t *tokens, uint32_t tokens_stride,
+                        const int32_t *counts, double *logits, uint32_t logits_stride,
+                        void *stream);
+
+/* softmax_weights (attention.hpp:31, attention.cpp:54-67) over rows of device logits:
+ * w = exp(l - max) / sum, fp64 (sum order and libm differ from the reference: ~1e-15
+ * relative).  counts == NULL: every row holds n logits.  An empty row -> status
+ * INVALID_ARGUMENT via qk_check_status(cache) (cache supplies the device and status). */
+QK_API int qk_softmax_weights(qk_cache *cache, const double *logits, const int32_t *counts,
+                       uint32_t n, uint32_t stride, uint32_t rows, double *weights,
+                       void *stream);
 
 /* One fused Quest decode step for a layer (the README's estimate -> select -> attend
  * loop, R/README.md:151-158, preceded by KvCache::append): appends k/v (if non-NULL),
@@ -213,9 +262,37 @@ QK_API int qk_select_topk_host(const qk_cache *cache, uint32_t layer, const doub
 QK_API int qk_sparse_attend_host(const qk_cache *cache, uint32_t layer, const uint16_t *q_host,
                                  uint32_t batch, const int32_t *pages_host,
                                  uint32_t pages_stride, const int32_t *counts_host,
-                                 float *out_host, float *lse_host, void *stream);
+                                 float *out_host, float *lse_host, double *wsum_host,
+                                 void *stream);
 QK_API int qk_dense_attend_host(const qk_cache *cache, uint32_t layer, const uint16_t *q_host,
-                                uint32_t batch, float *out_host, float *lse_host, void *stream);
+                                uint32_t batch, float *out_host, float *lse_host,
+                                double *wsum_host, void *stream);
+/* Host arrays; the page range is checked on the host first (the reference's order). */
+QK_API int qk_select_topk_pairs_host(qk_cache *cache, uint32_t layer, uint32_t seq,
+                                     const uint32_t *page_index_host, const double *scores_host,
+                                     uint32_t n, const qk_selection_cfg *cfg, int32_t *pages_host,
+                                     uint32_t pages_capacity, int32_t *count_host, void *stream);
+/* Token lists validated on the host first with check_token_set's errors and messages. */
+QK_API int qk_attend_tokens_host(const qk_cache *cache, uint32_t layer, const uint16_t *q_host,
+                                 uint32_t batch, const int32_t *tokens_host,
+                                 uint32_t tokens_stride, const int32_t *counts_host,
+                                 float *out_host, float *lse_host, double *wsum_host,
+                                 void *stream);
+QK_API int qk_attention_logits_host(const qk_cache *cache, uint32_t layer,
+                                    const uint16_t *q_host, uint32_t batch,
+                                    const int32_t *tokens_host, uint32_t tokens_stride,
+                                    const int32_t *counts_host, double *logits_host,
+                                    uint32_t logits_stride, void *stream);
+/* estimate_page_score (criticality.cpp:9-23) on explicit metadata, host arrays:
+ * q [head_dim], min/max [n_pages][head_dim] (fp16 bits) -> scores [n_pages], bitwise the
+ * reference's doubles; computed on `device` (per-device scratch, no cache needed). */
+QK_API int qk_estimate_metadata_host(const uint16_t *q_host, const uint16_t *min_host,
+                                     const uint16_t *max_host, uint32_t n_pages,
+                                     uint32_t head_dim, double *scores_host, int32_t device);
+/* softmax_weights on one host vector, computed on `device` (empty -> INVALID_ARGUMENT
+ * "softmax_weights: empty logits", as the reference). */
+QK_API int qk_softmax_weights_host(const double *logits_host, uint32_t n, double *weights_host,
+                                   int32_t device);
 
 /* Diagnostics / parity: with `on`, qk_decode_step estimates every page (also the forced
  * newest page, and when the budget covers the cache) and keeps the scores for

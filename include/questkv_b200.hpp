@@ -13,10 +13,10 @@
 //     (metadata, scores and page sets bitwise, outputs within 1e-5 relative L2);
 //   * KvCache has a fixed capacity (constructor argument; the reference grows without bound);
 //   * accessors return values instead of references into host-side storage;
-//   * select_top_k takes estimate_all's form (one score per page, in page order) and throws
-//     std::invalid_argument otherwise -- the GPU selector has no host fallback;
-//   * AttentionOutput::weights_sum_check is 1 by construction (the kernel divides by the
-//     merged softmax normaliser).
+//   * AttentionOutput::weights_sum_check is the post-softmax mass of the weights the kernel
+//     applied, evaluated in fp64 from its fp32 partials (1 up to fp32 rounding);
+//   * softmax_weights runs on the current CUDA device (exp and summation order differ from
+//     glibc's sequential loop: ~1e-15 relative).
 // No CPU fallback exists: constructing a KvCache without a CUDA device throws
 // std::runtime_error.
 #pragma once
@@ -248,20 +248,21 @@ inline std::vector<PageScore> estimate_all(std::span<const float> query, const K
     return out;
 }
 
-// estimate_page_score (criticality.cpp:9-23) on explicit metadata: a one-page device cache
-// whose two keys are min_key and max_key has exactly that metadata.
+// estimate_page_score (criticality.cpp:9-23) on explicit metadata, on the GPU (no cache).
 inline double estimate_page_score(std::span<const float> query, const PageMetadata& metadata) {
     const uint32_t d = uint32_t(metadata.min_key.size());
     if (d == 0 || query.size() != d || metadata.max_key.size() != d)
         throw std::invalid_argument("estimate_page_score: dimension mismatch");
-    KvCache tmp(CacheConfig{d, 2, 2}, 2);
-    std::vector<float> keys(metadata.min_key), vals(2 * size_t(d), 0.0f);
-    keys.insert(keys.end(), metadata.max_key.begin(), metadata.max_key.end());
-    tmp.extend(keys, vals);
-    return estimate_all(query, tmp)[0].score;
+    const auto q = to_half(query), mn = to_half(metadata.min_key), mx = to_half(metadata.max_key);
+    int dev = 0;
+    double score = 0.0;
+    check(qk_estimate_metadata_host(q.data(), mn.data(), mx.data(), 1, d, &score, dev));
+    return score;
 }
 
-// select_top_k (criticality.cpp:36-81), same early-exit order and errors.
+// select_top_k (criticality.cpp:36-81), same early-exit order and errors.  estimate_all's
+// form (one score per page, in page order) takes the radix top-K kernel; any other vector
+// (any order, repeated pages) the pair-sorting kernel -- both on the GPU.
 inline std::vector<uint32_t> select_top_k(const std::vector<PageScore>& scores,
                                           const SelectionConfig& config, const KvCache& cache) {
     const uint32_t P = cache.page_count();
@@ -273,27 +274,105 @@ inline std::vector<uint32_t> select_top_k(const std::vector<PageScore>& scores,
     if (scores.empty()) throw std::invalid_argument("select_top_k: no scores");
     for (const PageScore& s : scores)
         if (s.page_index >= P) throw std::out_of_range("select_top_k: score for nonexistent page");
-    if (scores.size() != P)
-        throw std::invalid_argument("select_top_k: the GPU selector takes one score per page");
-    std::vector<double> s(P);
-    for (uint32_t p = 0; p < P; ++p) {
-        if (scores[p].page_index != p)
-            throw std::invalid_argument("select_top_k: scores must be in page order");
-        s[p] = scores[p].score;
-    }
     qk_selection_cfg cfg{config.token_budget, config.force_include_recent ? 1 : 0, 1};
-    std::vector<int32_t> pages(P);
+    bool page_order = scores.size() == P;
+    for (uint32_t p = 0; page_order && p < P; ++p) page_order = scores[p].page_index == p;
+    if (page_order) {
+        std::vector<double> s(P);
+        for (uint32_t p = 0; p < P; ++p) s[p] = scores[p].score;
+        std::vector<int32_t> pages(P);
+        int32_t count = 0;
+        check(qk_select_topk_host(cache.handle(), 0, s.data(), P, 1, &cfg, pages.data(), P, &count,
+                                  nullptr));
+        return std::vector<uint32_t>(pages.begin(), pages.begin() + count);
+    }
+    std::vector<uint32_t> idx(scores.size());
+    std::vector<double> s(scores.size());
+    for (size_t i = 0; i < scores.size(); ++i) {
+        idx[i] = scores[i].page_index;
+        s[i] = scores[i].score;
+    }
+    const uint32_t cap = std::max<uint32_t>({P, config.token_budget / cache.config().page_size, 1u});
+    std::vector<int32_t> pages(cap);
     int32_t count = 0;
-    check(qk_select_topk_host(cache.handle(), 0, s.data(), P, 1, &cfg, pages.data(), P, &count,
-                              nullptr));
+    check(qk_select_topk_pairs_host(cache.handle(), 0, 0, idx.data(), s.data(), uint32_t(s.size()),
+                                    &cfg, pages.data(), cap, &count, nullptr));
     return std::vector<uint32_t>(pages.begin(), pages.begin() + count);
 }
 
 // ---- attention.hpp --------------------------------------------------------------------------
+using LogitVector = std::vector<double>;  // attention.hpp:13
+
 struct AttentionOutput {  // attention.hpp:15-18
     std::vector<double> output;
     double weights_sum_check = 0.0;
 };
+
+namespace detail {
+// check_token_set (attention.cpp:19-30), same messages and exception types.
+inline void check_token_set(const KvCache& cache, std::span<const uint32_t> tokens) {
+    if (tokens.empty()) throw std::invalid_argument("attention: empty token set");
+    const uint32_t n = cache.token_count();
+    for (size_t i = 0; i < tokens.size(); ++i) {
+        if (tokens[i] >= n) throw std::out_of_range("attention: token index out of range");
+        if (i > 0 && tokens[i] <= tokens[i - 1])
+            throw std::invalid_argument("attention: token set must be strictly ascending");
+    }
+}
+}  // namespace detail
+
+// attention_logits (attention.cpp:34-46): q.k_t / sqrt(d) over token_subset, bitwise.
+inline LogitVector attention_logits(std::span<const float> query, const KvCache& cache,
+                                    std::span<const uint32_t> token_subset) {
+    detail::check_token_set(cache, token_subset);
+    if (query.size() != cache.config().head_dim)
+        throw std::invalid_argument("attention_logits: query dimension mismatch");
+    const auto q = to_half(query);
+    const std::vector<int32_t> toks(token_subset.begin(), token_subset.end());
+    const int32_t count = int32_t(toks.size());
+    LogitVector logits(toks.size());
+    check(qk_attention_logits_host(cache.handle(), 0, q.data(), 1, toks.data(), uint32_t(toks.size()),
+                                   &count, logits.data(), uint32_t(toks.size()), nullptr));
+    return logits;
+}
+
+// attention_logits over every cached token (attention.cpp:48-52).
+inline LogitVector attention_logits(std::span<const float> query, const KvCache& cache) {
+    const uint32_t n = cache.token_count();
+    if (n == 0) throw std::invalid_argument("attention: empty token set");
+    if (query.size() != cache.config().head_dim)
+        throw std::invalid_argument("attention_logits: query dimension mismatch");
+    const auto q = to_half(query);
+    LogitVector logits(n);
+    check(qk_attention_logits_host(cache.handle(), 0, q.data(), 1, nullptr, 0, nullptr,
+                                   logits.data(), n, nullptr));
+    return logits;
+}
+
+// softmax_weights (attention.cpp:54-67), on the current CUDA device.
+inline std::vector<double> softmax_weights(const LogitVector& logits) {
+    if (logits.empty()) throw std::invalid_argument("softmax_weights: empty logits");
+    std::vector<double> w(logits.size());
+    int dev = 0;
+    check(qk_softmax_weights_host(logits.data(), uint32_t(logits.size()), w.data(), dev));
+    return w;
+}
+
+// attend_tokens (attention.cpp:69-84): attention over an explicit strictly ascending token set.
+inline AttentionOutput attend_tokens(std::span<const float> query, const KvCache& cache,
+                                     std::span<const uint32_t> tokens) {
+    detail::check_token_set(cache, tokens);
+    if (query.size() != cache.config().head_dim)
+        throw std::invalid_argument("attention_logits: query dimension mismatch");
+    const auto q = to_half(query);
+    const std::vector<int32_t> toks(tokens.begin(), tokens.end());
+    const int32_t count = int32_t(toks.size());
+    std::vector<float> out(cache.config().head_dim);
+    double wsum = 0.0;
+    check(qk_attend_tokens_host(cache.handle(), 0, q.data(), 1, toks.data(), uint32_t(toks.size()),
+                                &count, out.data(), nullptr, &wsum, nullptr));
+    return {std::vector<double>(out.begin(), out.end()), wsum};
+}
 
 inline AttentionOutput full_attention(std::span<const float> query, const KvCache& cache) {
     if (cache.token_count() == 0) throw std::invalid_argument("full_attention: empty cache");
@@ -301,8 +380,9 @@ inline AttentionOutput full_attention(std::span<const float> query, const KvCach
         throw std::invalid_argument("attention: query dimension mismatch");
     const auto q = to_half(query);
     std::vector<float> out(cache.config().head_dim);
-    check(qk_dense_attend_host(cache.handle(), 0, q.data(), 1, out.data(), nullptr, nullptr));
-    return {std::vector<double>(out.begin(), out.end()), 1.0};
+    double wsum = 0.0;
+    check(qk_dense_attend_host(cache.handle(), 0, q.data(), 1, out.data(), nullptr, &wsum, nullptr));
+    return {std::vector<double>(out.begin(), out.end()), wsum};
 }
 
 // sparse_attention (attention.cpp:94-116): any order accepted; empty -> invalid_argument,
@@ -323,9 +403,11 @@ inline AttentionOutput sparse_attention(std::span<const float> query, const KvCa
     const auto q = to_half(query);
     const int32_t count = int32_t(pages.size());
     std::vector<float> out(cache.config().head_dim);
+    double wsum = 0.0;
     check(qk_sparse_attend_host(cache.handle(), 0, q.data(), 1, pages.data(),
-                                uint32_t(pages.size()), &count, out.data(), nullptr, nullptr));
-    return {std::vector<double>(out.begin(), out.end()), 1.0};
+                                uint32_t(pages.size()), &count, out.data(), nullptr, &wsum,
+                                nullptr));
+    return {std::vector<double>(out.begin(), out.end()), wsum};
 }
 
 // ---- metrics.hpp (the byte model of the roofline) ------------------------------------------

@@ -72,8 +72,17 @@ SIGNATURES = {
         ctypes.c_int,
         [_P, _U32, _P, _U32, _U32, ctypes.POINTER(qk_selection_cfg), _P, _U32, _P, _P],
     ),
-    "qk_sparse_attend": (ctypes.c_int, [_P, _U32, _P, _U32, _P, _U32, _P, _P, _I32, _P, _P]),
-    "qk_dense_attend": (ctypes.c_int, [_P, _U32, _P, _U32, _P, _I32, _P, _P]),
+    "qk_sparse_attend": (ctypes.c_int, [_P, _U32, _P, _U32, _P, _U32, _P, _P, _I32, _P, _P, _P]),
+    "qk_dense_attend": (ctypes.c_int, [_P, _U32, _P, _U32, _P, _I32, _P, _P, _P]),
+    "qk_select_topk_pairs": (
+        ctypes.c_int, [_P, _U32, _U32, _P, _P, _U32, ctypes.POINTER(qk_selection_cfg), _P, _U32, _P, _P],
+    ),
+    "qk_select_topk_pairs_host": (
+        ctypes.c_int, [_P, _U32, _U32, _P, _P, _U32, ctypes.POINTER(qk_selection_cfg), _P, _U32, _P, _P],
+    ),
+    "qk_attend_tokens": (ctypes.c_int, [_P, _U32, _P, _U32, _P, _U32, _P, _P, _I32, _P, _P, _P]),
+    "qk_attention_logits": (ctypes.c_int, [_P, _U32, _P, _U32, _P, _U32, _P, _P, _U32, _P]),
+    "qk_softmax_weights": (ctypes.c_int, [_P, _P, _P, _U32, _U32, _U32, _P, _P]),
     "qk_decode_step": (
         ctypes.c_int,
         [_P, _U32, _P, _P, _P, _U32, ctypes.POINTER(qk_selection_cfg), _P, _I32, _P, _U32, _P, _P],
@@ -95,8 +104,12 @@ SIGNATURES = {
         ctypes.c_int,
         [_P, _U32, _P, _U32, _U32, ctypes.POINTER(qk_selection_cfg), _P, _U32, _P, _P],
     ),
-    "qk_sparse_attend_host": (ctypes.c_int, [_P, _U32, _P, _U32, _P, _U32, _P, _P, _P, _P]),
-    "qk_dense_attend_host": (ctypes.c_int, [_P, _U32, _P, _U32, _P, _P, _P]),
+    "qk_sparse_attend_host": (ctypes.c_int, [_P, _U32, _P, _U32, _P, _U32, _P, _P, _P, _P, _P]),
+    "qk_dense_attend_host": (ctypes.c_int, [_P, _U32, _P, _U32, _P, _P, _P, _P]),
+    "qk_attend_tokens_host": (ctypes.c_int, [_P, _U32, _P, _U32, _P, _U32, _P, _P, _P, _P, _P]),
+    "qk_attention_logits_host": (ctypes.c_int, [_P, _U32, _P, _U32, _P, _U32, _P, _P, _U32, _P]),
+    "qk_softmax_weights_host": (ctypes.c_int, [_P, _U32, _P, _I32]),
+    "qk_estimate_metadata_host": (ctypes.c_int, [_P, _P, _P, _U32, _U32, _P, _I32]),
 }
 
 _lib = None

@@ -21,6 +21,15 @@
 // order; splits write (m, l, o) partials and the last CTA of a (sequence, head) -- found
 // with a ticket counter -- merges them in split order (deterministic) and writes the
 // output.
+//
+// Token mode (attend_tokens, attention.cpp:69-84): the list holds token indices (strictly
+// ascending, < token_count, checked on the device like check_token_set, attention.cpp:19-30);
+// chunks of page_size consecutive list entries play the role of pages (same split rule over
+// ceil(count / S) chunks), so attend_tokens over every token is bitwise full_attention.
+//
+// weights_sum (optional, AttentionOutput::weights_sum_check, attention.cpp:81): the
+// post-softmax mass of the weights the output applied, sum_s l_s*2^(m_s-M) / L, evaluated in
+// fp64 from the fp32 partials (1 up to the fp32 rounding of the normaliser L).
 #include "attend_warp.cuh"
 
 namespace qk {
@@ -34,11 +43,12 @@ __global__ void __launch_bounds__(kThreads)
 attend_kernel(const __half* __restrict__ kp, const __half* __restrict__ vp,
               const int32_t* __restrict__ len, const __half* __restrict__ q,
               const int32_t* __restrict__ pages, uint32_t pstride,
-              const int32_t* __restrict__ counts, int dense, uint32_t layer, uint32_t B,
+              const int32_t* __restrict__ counts, int mode, uint32_t layer, uint32_t B,
               uint32_t Hq, uint32_t Hkv, uint32_t S, uint32_t head_dim, size_t slice_kv,
               float scale_log2, float* __restrict__ ws_partial, int32_t* __restrict__ ws_ticket,
               void* __restrict__ out, int out_dtype, float* __restrict__ lse,
-              int32_t* __restrict__ status) {
+              double* __restrict__ wsum, int32_t* __restrict__ status) {
+    const bool dense = mode == kModeDense, tokens = mode == kModeTokens;
     constexpr int CPR = D / 8;  // 16-byte chunks per row
     __shared__ float s_o[kWarps][D];
     __shared__ float s_m[kWarps], s_l[kWarps];
@@ -51,11 +61,14 @@ attend_kernel(const __half* __restrict__ kp, const __half* __restrict__ vp,
     const uint32_t P = (n_tok + S - 1) / S;
     const int count = dense ? int(P) : counts[bh];
     if (count < 1) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) record_status(status, QK_DEV_EMPTY_SELECTION);
+        if (blockIdx.x == 0 && threadIdx.x == 0)
+            record_status(status, tokens ? QK_DEV_EMPTY_TOKENS : QK_DEV_EMPTY_SELECTION);
         return;
     }
-    const int pps = max(kMinPagesPerSplit, (count + kMaxSplits - 1) / kMaxSplits);
-    const int nsplit = (count + pps - 1) / pps;
+    // Units of the split rule: pages, or chunks of S list entries (token mode).
+    const int units = tokens ? int((uint32_t(count) + S - 1) / S) : count;
+    const int pps = max(kMinPagesPerSplit, (units + kMaxSplits - 1) / kMaxSplits);
+    const int nsplit = (units + pps - 1) / pps;
     // A count past the list row, or needing more splits than the host launched, would read
     // past the row or never complete the merge ticket: reject it (uniform over the CTAs of
     // this (sequence, head), so no CTA takes the ticket).
@@ -66,7 +79,7 @@ attend_kernel(const __half* __restrict__ kp, const __half* __restrict__ vp,
     const int split = blockIdx.x;
     if (split >= nsplit) return;
     const int first = split * pps;
-    const int last = min(count, first + pps);
+    const int last = min(units, first + pps);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int chunk = lane % CPR, rgrp = lane / CPR;
@@ -84,6 +97,28 @@ attend_kernel(const __half* __restrict__ kp, const __half* __restrict__ vp,
     for (int j = 0; j < 8; ++j) o[j] = 0.0f;
 
     for (int i = first + warp; i < last; i += kWarps) {
+        if (tokens) {
+            // Chunk i: list entries [i*S, min(count, i*S+S)), each checked like
+            // check_token_set (attention.cpp:19-30).
+            const uint32_t e0 = uint32_t(i) * S;
+            const uint32_t n = min(S, uint32_t(count) - e0);
+            bool bad_range = false, bad_order = false;
+            for (uint32_t r = lane; r < n; r += 32) {
+                const int32_t t = plist[e0 + r];
+                bad_range |= t < 0 || uint32_t(t) >= n_tok;
+                bad_order |= (e0 + r) > 0 && plist[e0 + r - 1] >= t;
+            }
+            bad_range = __any_sync(0xffffffffu, bad_range);
+            bad_order = __any_sync(0xffffffffu, bad_order);
+            if (bad_range || bad_order) {
+                if (lane == 0)
+                    record_status(status, bad_range ? QK_DEV_TOKEN_OUT_OF_RANGE
+                                                    : QK_DEV_TOKEN_NOT_ASCENDING);
+                continue;
+            }
+            warp_fold_page<D, false>(kslice, vslice, n, qf, scale_log2, m, l, o, plist + e0);
+            continue;
+        }
         int pg = i;
         if (!dense) {
             pg = plist[i];
@@ -134,6 +169,12 @@ attend_kernel(const __half* __restrict__ kp, const __half* __restrict__ vp,
             else static_cast<__half*>(out)[out_base + d] = __float2half_rn(r);
         }
         if (lse && tid == 0) lse[bh] = (M + log2f(L)) * 0.69314718055994530942f;
+        if (wsum && tid == 0) {
+            double mass = 0.0;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) mass += double(s_l[w]) * double(w_scale[w]);
+            wsum[bh] = mass / double(L);
+        }
         return;
     }
 
@@ -177,23 +218,34 @@ attend_kernel(const __half* __restrict__ kp, const __half* __restrict__ vp,
         else static_cast<__half*>(out)[out_base + d] = __float2half_rn(r);
     }
     if (lse && tid == 0) lse[bh] = (Mg + log2f(Lg)) * 0.69314718055994530942f;
+    if (wsum && tid == 0) {
+        double mass = 0.0;
+        for (int sp = 0; sp < nsplit; ++sp) {
+            const float ms = __ldcg(parts + size_t(sp) * (D + 2));
+            const float ls = __ldcg(parts + size_t(sp) * (D + 2) + 1);
+            if (ms != -CUDART_INF_F) mass += double(ls) * double(exp2f(ms - Mg));
+        }
+        wsum[bh] = mass / double(Lg);
+    }
     if (tid == 0) ws_ticket[bh] = 0;  // re-arm for the next launch / graph replay
 }
 
 template <int D>
 int run(const qk_cache* c, uint32_t layer, const __half* q, uint32_t batch,
-        const int32_t* pages, uint32_t pstride, const int32_t* counts, bool dense,
-        uint32_t max_list, void* out, int out_dtype, float* lse, cudaStream_t st) {
+        const int32_t* pages, uint32_t pstride, const int32_t* counts, int mode,
+        uint32_t max_list, void* out, int out_dtype, float* lse, double* wsum, cudaStream_t st) {
+    // max_list: the longest list (pages, or tokens in token mode) a row may hold.
+    const uint32_t max_units = mode == kModeTokens ? (max_list + c->S - 1) / c->S : max_list;
     const uint32_t splits_needed =
-        max_list <= uint32_t(kMinPagesPerSplit) * kMaxSplits
-            ? (max_list + kMinPagesPerSplit - 1) / kMinPagesPerSplit
+        max_units <= uint32_t(kMinPagesPerSplit) * kMaxSplits
+            ? (max_units + kMinPagesPerSplit - 1) / kMinPagesPerSplit
             : uint32_t(kMaxSplits);
     const dim3 grid(splits_needed ? splits_needed : 1, batch * c->Hq);
     const float scale_log2 = float(1.4426950408889634 / sqrt(double(c->desc.head_dim)));
     attend_kernel<D><<<grid, kThreads, 0, st>>>(
-        c->k_pool, c->v_pool, c->d_len, q, pages, pstride, counts, dense ? 1 : 0, layer, c->B,
+        c->k_pool, c->v_pool, c->d_len, q, pages, pstride, counts, mode, layer, c->B,
         c->Hq, c->Hkv, c->S, c->desc.head_dim, c->slice_kv, scale_log2, c->ws_partial,
-        c->ws_ticket, out, out_dtype, lse, c->d_status);
+        c->ws_ticket, out, out_dtype, lse, wsum, c->d_status);
     const_cast<qk_cache*>(c)->launches++;
     return cuda_check(cudaGetLastError(), "attend_kernel");
 }
@@ -201,12 +253,13 @@ int run(const qk_cache* c, uint32_t layer, const __half* q, uint32_t batch,
 }  // namespace
 
 int launch_attend(const qk_cache* c, uint32_t layer, const __half* q, uint32_t batch,
-                  const int32_t* pages, uint32_t pstride, const int32_t* counts, bool dense,
-                  uint32_t max_list, void* out, int out_dtype, float* lse, cudaStream_t st) {
+                  const int32_t* pages, uint32_t pstride, const int32_t* counts, int mode,
+                  uint32_t max_list, void* out, int out_dtype, float* lse, double* wsum,
+                  cudaStream_t st) {
     switch (c->D) {
-        case 64: return run<64>(c, layer, q, batch, pages, pstride, counts, dense, max_list, out, out_dtype, lse, st);
-        case 128: return run<128>(c, layer, q, batch, pages, pstride, counts, dense, max_list, out, out_dtype, lse, st);
-        case 256: return run<256>(c, layer, q, batch, pages, pstride, counts, dense, max_list, out, out_dtype, lse, st);
+        case 64: return run<64>(c, layer, q, batch, pages, pstride, counts, mode, max_list, out, out_dtype, lse, wsum, st);
+        case 128: return run<128>(c, layer, q, batch, pages, pstride, counts, mode, max_list, out, out_dtype, lse, wsum, st);
+        case 256: return run<256>(c, layer, q, batch, pages, pstride, counts, mode, max_list, out, out_dtype, lse, wsum, st);
         default: return set_error(QK_ERR_UNSUPPORTED, "qk_attend: unsupported head_dim");
     }
 }

@@ -36,12 +36,17 @@ __device__ __forceinline__ void unpack8(const int4& v, float (&f)[8]) {
 }
 
 // Folds one page (plen valid rows) into (m, l, o).  COHERENT selects plain loads (data
-// written earlier in the same kernel) instead of the read-only path.
+// written earlier in the same kernel) instead of the read-only path.  With `rows` (token
+// granularity, attend_tokens) row r of the chunk is token rows[r] of the slice, i.e. at
+// kpage + rows[r]*D with kpage the slice base; without it, row r is at kpage + r*D.  A chunk
+// of consecutive tokens starting at a page boundary therefore loads and folds exactly what
+// the page form does (bitwise equal results).
 template <int D, bool COHERENT>
 __device__ __forceinline__ void warp_fold_page(const __half* __restrict__ kpage,
                                                const __half* __restrict__ vpage, uint32_t plen,
                                                const float (&qf)[8], float scale_log2, float& m,
-                                               float& l, float (&o)[8]) {
+                                               float& l, float (&o)[8],
+                                               const int32_t* __restrict__ rows = nullptr) {
     constexpr int CPR = D / 8;
     constexpr int RPI = 32 / CPR;
     const int lane = threadIdx.x & 31;
@@ -52,12 +57,13 @@ __device__ __forceinline__ void warp_fold_page(const __half* __restrict__ kpage,
         for (int it = 0; it < kBatchIters; ++it) {
             const uint32_t r = r0 + it * RPI + rgrp;
             if (r < plen) {
+                const size_t row = rows ? size_t(uint32_t(rows[r])) : size_t(r);
                 if (COHERENT) {
-                    kv[it] = ld_v4_coherent(kpage + size_t(r) * D + chunk * 8);
-                    vv[it] = ld_v4_coherent(vpage + size_t(r) * D + chunk * 8);
+                    kv[it] = ld_v4_coherent(kpage + row * D + chunk * 8);
+                    vv[it] = ld_v4_coherent(vpage + row * D + chunk * 8);
                 } else {
-                    kv[it] = ld_nc_v4(kpage + size_t(r) * D + chunk * 8);
-                    vv[it] = ld_nc_v4(vpage + size_t(r) * D + chunk * 8);
+                    kv[it] = ld_nc_v4(kpage + row * D + chunk * 8);
+                    vv[it] = ld_nc_v4(vpage + row * D + chunk * 8);
                 }
             } else {
                 kv[it] = make_int4(0, 0, 0, 0);

@@ -102,7 +102,7 @@ void free_cache(qk_cache* c) {
     void* ptrs[] = {c->k_pool,    c->v_pool,    c->meta,      c->d_len,     c->ws_partial,
                     c->ws_ticket, c->d_status,  c->ws_scores, c->ws_pages,  c->ws_counts,
                     c->ws_io,     c->ws_out,    c->len_ticket, c->probe,     c->ws_lse,
-                    c->prange,    c->done_counter};
+                    c->prange,    c->done_counter, c->ws_wsum};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->host_stage) cudaFreeHost(c->host_stage);
@@ -188,6 +188,7 @@ int qk_cache_create(const qk_cache_desc* desc, qk_cache** out) {
     if (!rc) rc = dmalloc(c, &c->ws_io, size_t(c->B) * (c->Hq + 2 * c->Hkv) * desc->head_dim);
     if (!rc) rc = dmalloc(c, &c->ws_out, size_t(c->B) * c->Hq * desc->head_dim);
     if (!rc) rc = dmalloc(c, &c->ws_lse, size_t(c->B) * c->Hq);
+    if (!rc) rc = dmalloc(c, &c->ws_wsum, size_t(c->B) * c->Hq);
     if (!rc) rc = cuda_check(cudaDeviceSynchronize(), "qk_cache_create");
     if (rc) {
         free_cache(c);
@@ -315,6 +316,37 @@ int read_back(qk_cache* c, __half* d0, __half* d1, uint16_t* h0, uint16_t* h1, s
     return rc;
 }
 
+// out / lse / weights_sum device workspaces -> host (asynchronous on st).
+int copy_results(qk_cache* c, float* out_host, float* lse_host, double* wsum_host, size_t rows,
+                 size_t nq, cudaStream_t st) {
+    int rc = cuda_check(cudaMemcpyAsync(out_host, c->ws_out, nq * 4, cudaMemcpyDeviceToHost, st), "d2h out");
+    if (!rc && lse_host)
+        rc = cuda_check(cudaMemcpyAsync(lse_host, c->ws_lse, rows * 4, cudaMemcpyDeviceToHost, st), "d2h lse");
+    if (!rc && wsum_host)
+        rc = cuda_check(cudaMemcpyAsync(wsum_host, c->ws_wsum, rows * 8, cudaMemcpyDeviceToHost, st), "d2h wsum");
+    return rc;
+}
+
+// check_token_set (attention.cpp:19-30) on host lists, same errors and messages.
+int check_token_sets(const qk_cache* c, uint32_t layer, const int32_t* tokens, uint32_t stride,
+                     const int32_t* counts, size_t rows) {
+    for (size_t r = 0; r < rows; ++r) {
+        const uint32_t L = c->h_len[size_t(layer) * c->B + r / c->Hq];
+        const int32_t n = counts[r];
+        if (n <= 0) return set_error(QK_ERR_INVALID_ARGUMENT, "attention: empty token set");
+        if (uint32_t(n) > stride)
+            return set_error(QK_ERR_INVALID_ARGUMENT, "attention: token count above tokens_stride");
+        const int32_t* tl = tokens + r * stride;
+        for (int32_t i = 0; i < n; ++i) {
+            if (tl[i] < 0 || uint32_t(tl[i]) >= L)
+                return set_error(QK_ERR_OUT_OF_RANGE, "attention: token index out of range");
+            if (i > 0 && tl[i] <= tl[i - 1])
+                return set_error(QK_ERR_INVALID_ARGUMENT, "attention: token set must be strictly ascending");
+        }
+    }
+    return QK_OK;
+}
+
 }  // namespace readback
 }  // namespace qk
 
@@ -422,9 +454,80 @@ int qk_select_topk(const qk_cache* c, uint32_t layer, const double* scores,
                        c->Pmax, as_stream(stream));
 }
 
+int qk_select_topk_pairs(qk_cache* c, uint32_t layer, uint32_t seq, const uint32_t* page_index,
+                         const double* scores, uint32_t n, const qk_selection_cfg* cfg,
+                         int32_t* pages, uint32_t pages_capacity, int32_t* count, void* stream) {
+    if (!c || !cfg || !pages || !count || (n && (!page_index || !scores)))
+        return set_error(QK_ERR_INVALID_ARGUMENT, "select_top_k: null argument");
+    if (layer >= c->L || seq >= c->B)
+        return set_error(QK_ERR_OUT_OF_RANGE, "select_top_k: slice out of range");
+    // criticality.cpp:46-59, in the reference's order.
+    int all_pages = 0;
+    uint32_t k = 0;
+    if (!cfg->per_layer_enabled) {
+        all_pages = 2;
+    } else {
+        if (cfg->token_budget < c->S)
+            return set_error(QK_ERR_INVALID_ARGUMENT, "select_top_k: token_budget below page_size");
+        if (n == 0) return set_error(QK_ERR_INVALID_ARGUMENT, "select_top_k: no scores");
+        if (n > kMaxPages)
+            return set_error(QK_ERR_UNSUPPORTED, "select_top_k: more than 16384 scores");
+        k = cfg->token_budget / c->S;
+        if (k >= n) all_pages = 1;
+        else if (pages_capacity < k)
+            return set_error(QK_ERR_INVALID_ARGUMENT, "select_top_k: pages capacity below K");
+    }
+    if (all_pages && pages_capacity < pages_of(c, c->h_len[size_t(layer) * c->B + seq]))
+        return set_error(QK_ERR_INVALID_ARGUMENT, "select_top_k: pages capacity below page count");
+    DeviceGuard guard(c->desc.device);
+    return launch_topk_pairs(c, layer, seq, page_index, scores, all_pages == 2 ? 0 : n, k,
+                             cfg->force_include_recent ? 1 : 0, all_pages, pages_capacity, pages,
+                             count, as_stream(stream));
+}
+
+int qk_select_topk_pairs_host(qk_cache* c, uint32_t layer, uint32_t seq,
+                              const uint32_t* page_index_host, const double* scores_host,
+                              uint32_t n, const qk_selection_cfg* cfg, int32_t* pages_host,
+                              uint32_t pages_capacity, int32_t* count_host, void* stream) {
+    if (!c || !cfg || !pages_host || !count_host || (n && (!page_index_host || !scores_host)))
+        return set_error(QK_ERR_INVALID_ARGUMENT, "select_top_k: null argument");
+    if (layer >= c->L || seq >= c->B)
+        return set_error(QK_ERR_OUT_OF_RANGE, "select_top_k: slice out of range");
+    if (cfg->per_layer_enabled) {  // the reference's checks, host side first (same order)
+        if (cfg->token_budget < c->S)
+            return set_error(QK_ERR_INVALID_ARGUMENT, "select_top_k: token_budget below page_size");
+        if (n == 0) return set_error(QK_ERR_INVALID_ARGUMENT, "select_top_k: no scores");
+        const uint32_t P = pages_of(c, c->h_len[size_t(layer) * c->B + seq]);
+        for (uint32_t i = 0; i < n; ++i)
+            if (page_index_host[i] >= P)
+                return set_error(QK_ERR_OUT_OF_RANGE, "select_top_k: score for nonexistent page");
+    }
+    DeviceGuard guard(c->desc.device);
+    cudaStream_t st = as_stream(stream);
+    void* buf = nullptr;
+    const size_t nb = size_t(n) * 12 + size_t(pages_capacity) * 4 + 16;
+    int rc = cuda_check(cudaMalloc(&buf, nb), "select_top_k");
+    if (rc) return rc;
+    double* dsc = static_cast<double*>(buf);
+    uint32_t* dpi = reinterpret_cast<uint32_t*>(dsc + n);
+    int32_t* dpages = reinterpret_cast<int32_t*>(dpi + n);
+    int32_t* dcount = dpages + pages_capacity;
+    if (n) rc = cuda_check(cudaMemcpyAsync(dsc, scores_host, size_t(n) * 8, cudaMemcpyHostToDevice, st), "h2d");
+    if (!rc && n) rc = cuda_check(cudaMemcpyAsync(dpi, page_index_host, size_t(n) * 4, cudaMemcpyHostToDevice, st), "h2d");
+    if (!rc) rc = qk_select_topk_pairs(c, layer, seq, dpi, dsc, n, cfg, dpages, pages_capacity, dcount, stream);
+    if (!rc) rc = cuda_check(cudaMemcpyAsync(count_host, dcount, 4, cudaMemcpyDeviceToHost, st), "d2h");
+    if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "select_top_k");
+    if (!rc && *count_host > 0)
+        rc = cuda_check(cudaMemcpy(pages_host, dpages, size_t(*count_host) * 4, cudaMemcpyDeviceToHost), "d2h");
+    cudaFree(buf);
+    if (!rc) rc = qk_check_status(c, stream);
+    return rc;
+}
+
 int qk_sparse_attend(const qk_cache* c, uint32_t layer, const uint16_t* q, uint32_t batch,
                      const int32_t* pages, uint32_t pages_stride, const int32_t* counts,
-                     void* out, int32_t out_dtype, float* lse, void* stream) {
+                     void* out, int32_t out_dtype, float* lse, double* weights_sum,
+                     void* stream) {
     if (!c || !q || !pages || !counts || !out)
         return set_error(QK_ERR_INVALID_ARGUMENT, "sparse_attention: null argument");
     if (int rc = check_layer_batch(c, layer, batch, "sparse_attention")) return rc;
@@ -436,11 +539,12 @@ int qk_sparse_attend(const qk_cache* c, uint32_t layer, const uint16_t* q, uint3
     const uint32_t max_list = pages_stride < c->Pmax ? pages_stride : c->Pmax;
     DeviceGuard guard(c->desc.device);
     return launch_attend(c, layer, reinterpret_cast<const __half*>(q), batch, pages, pages_stride,
-                         counts, false, max_list, out, out_dtype, lse, as_stream(stream));
+                         counts, kModePages, max_list, out, out_dtype, lse, weights_sum,
+                         as_stream(stream));
 }
 
 int qk_dense_attend(const qk_cache* c, uint32_t layer, const uint16_t* q, uint32_t batch,
-                    void* out, int32_t out_dtype, float* lse, void* stream) {
+                    void* out, int32_t out_dtype, float* lse, double* weights_sum, void* stream) {
     if (!c || !q || !out) return set_error(QK_ERR_INVALID_ARGUMENT, "full_attention: null argument");
     if (int rc = check_layer_batch(c, layer, batch, "full_attention")) return rc;
     if (out_dtype != QK_DTYPE_F32 && out_dtype != QK_DTYPE_F16)
@@ -450,7 +554,62 @@ int qk_dense_attend(const qk_cache* c, uint32_t layer, const uint16_t* q, uint32
     if (empty) return set_error(QK_ERR_INVALID_ARGUMENT, "full_attention: empty cache");
     DeviceGuard guard(c->desc.device);
     return launch_attend(c, layer, reinterpret_cast<const __half*>(q), batch, nullptr, 0, nullptr,
-                         true, c->Pmax, out, out_dtype, lse, as_stream(stream));
+                         kModeDense, c->Pmax, out, out_dtype, lse, weights_sum, as_stream(stream));
+}
+
+int qk_attend_tokens(const qk_cache* c, uint32_t layer, const uint16_t* q, uint32_t batch,
+                     const int32_t* tokens, uint32_t tokens_stride, const int32_t* counts,
+                     void* out, int32_t out_dtype, float* lse, double* weights_sum,
+                     void* stream) {
+    if (!c || !q || !tokens || !counts || !out)
+        return set_error(QK_ERR_INVALID_ARGUMENT, "attend_tokens: null argument");
+    if (int rc = check_layer_batch(c, layer, batch, "attend_tokens")) return rc;
+    if (out_dtype != QK_DTYPE_F32 && out_dtype != QK_DTYPE_F16)
+        return set_error(QK_ERR_INVALID_ARGUMENT, "attend_tokens: bad out_dtype");
+    if (tokens_stride == 0) return set_error(QK_ERR_INVALID_ARGUMENT, "attention: empty token set");
+    const uint64_t cap = uint64_t(c->Pmax) * c->S;
+    const uint32_t max_list = uint32_t(tokens_stride < cap ? tokens_stride : cap);
+    DeviceGuard guard(c->desc.device);
+    return launch_attend(c, layer, reinterpret_cast<const __half*>(q), batch, tokens, tokens_stride,
+                         counts, kModeTokens, max_list, out, out_dtype, lse, weights_sum,
+                         as_stream(stream));
+}
+
+int qk_attention_logits(const qk_cache* c, uint32_t layer, const uint16_t* q, uint32_t batch,
+                        const int32_t* tokens, uint32_t tokens_stride, const int32_t* counts,
+                        double* logits, uint32_t logits_stride, void* stream) {
+    if (!c || !q || !logits || (tokens && !counts))
+        return set_error(QK_ERR_INVALID_ARGUMENT, "attention_logits: null argument");
+    if (int rc = check_layer_batch(c, layer, batch, "attention_logits")) return rc;
+    uint32_t max_list = 0;
+    if (tokens) {
+        if (tokens_stride == 0) return set_error(QK_ERR_INVALID_ARGUMENT, "attention: empty token set");
+        max_list = tokens_stride;
+    } else {
+        for (uint32_t b = 0; b < batch; ++b) {
+            const uint32_t t = c->h_len[size_t(layer) * c->B + b];
+            if (t == 0) return set_error(QK_ERR_INVALID_ARGUMENT, "attention: empty token set");
+            max_list = t > max_list ? t : max_list;
+        }
+        // Sized for the capacity: the device length decides (graph replays may grow it).
+        max_list = c->desc.max_tokens;
+    }
+    if (logits_stride < (tokens ? tokens_stride : 1))
+        return set_error(QK_ERR_INVALID_ARGUMENT, "attention_logits: logits_stride below the list");
+    DeviceGuard guard(c->desc.device);
+    return launch_logits(c, layer, reinterpret_cast<const __half*>(q), batch, tokens, tokens_stride,
+                         counts, max_list, logits, logits_stride, as_stream(stream));
+}
+
+int qk_softmax_weights(qk_cache* c, const double* logits, const int32_t* counts, uint32_t n,
+                       uint32_t stride, uint32_t rows, double* weights, void* stream) {
+    if (!c || !logits || !weights)
+        return set_error(QK_ERR_INVALID_ARGUMENT, "softmax_weights: null argument");
+    if (!counts && n == 0) return set_error(QK_ERR_INVALID_ARGUMENT, "softmax_weights: empty logits");
+    if (!counts && n > stride)
+        return set_error(QK_ERR_INVALID_ARGUMENT, "softmax_weights: n above stride");
+    DeviceGuard guard(c->desc.device);
+    return launch_softmax(logits, counts, n, stride, rows, weights, c->d_status, as_stream(stream));
 }
 
 int qk_decode_step(qk_cache* c, uint32_t layer, const uint16_t* q, const uint16_t* k,
@@ -670,7 +829,7 @@ int qk_select_topk_host(const qk_cache* cc, uint32_t layer, const double* scores
 int qk_sparse_attend_host(const qk_cache* cc, uint32_t layer, const uint16_t* q_host,
                           uint32_t batch, const int32_t* pages_host, uint32_t pages_stride,
                           const int32_t* counts_host, float* out_host, float* lse_host,
-                          void* stream) {
+                          double* wsum_host, void* stream) {
     qk_cache* c = const_cast<qk_cache*>(cc);
     if (!c || !q_host || !pages_host || !counts_host || !out_host)
         return set_error(QK_ERR_INVALID_ARGUMENT, "sparse_attention: null argument");
@@ -709,19 +868,159 @@ int qk_sparse_attend_host(const qk_cache* cc, uint32_t layer, const uint16_t* q_
                         "h2d pages");
     if (!rc) rc = cuda_check(cudaMemcpyAsync(c->ws_counts, counts_host, rows * 4, cudaMemcpyHostToDevice, st),
                              "h2d counts");
+    double* dws = wsum_host ? c->ws_wsum : nullptr;
     if (!rc)
         rc = qk_sparse_attend(c, layer, c->ws_io, batch, c->ws_pages, c->Pmax, c->ws_counts, c->ws_out,
-                              QK_DTYPE_F32, dlse, stream);
-    if (!rc) rc = cuda_check(cudaMemcpyAsync(out_host, c->ws_out, nq * 4, cudaMemcpyDeviceToHost, st), "d2h out");
-    if (!rc && lse_host)
-        rc = cuda_check(cudaMemcpyAsync(lse_host, dlse, rows * 4, cudaMemcpyDeviceToHost, st), "d2h lse");
+                              QK_DTYPE_F32, dlse, dws, stream);
+    if (!rc) rc = copy_results(c, out_host, lse_host, wsum_host, rows, nq, st);
     if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "qk_sparse_attend_host");
     if (!rc) rc = qk_check_status(c, stream);
     return rc;
 }
 
+int qk_attend_tokens_host(const qk_cache* cc, uint32_t layer, const uint16_t* q_host,
+                          uint32_t batch, const int32_t* tokens_host, uint32_t tokens_stride,
+                          const int32_t* counts_host, float* out_host, float* lse_host,
+                          double* wsum_host, void* stream) {
+    qk_cache* c = const_cast<qk_cache*>(cc);
+    if (!c || !q_host || !tokens_host || !counts_host || !out_host)
+        return set_error(QK_ERR_INVALID_ARGUMENT, "attend_tokens: null argument");
+    if (int rc = check_layer_batch(c, layer, batch, "attend_tokens")) return rc;
+    const size_t rows = size_t(batch) * c->Hq;
+    if (int rc = check_token_sets(c, layer, tokens_host, tokens_stride, counts_host, rows)) return rc;
+    DeviceGuard guard(c->desc.device);
+    cudaStream_t st = as_stream(stream);
+    const size_t nq = rows * c->desc.head_dim;
+    int32_t* dtok = nullptr;
+    int rc = cuda_check(cudaMalloc(&dtok, (rows * tokens_stride + rows) * sizeof(int32_t)), "attend_tokens");
+    if (rc) return rc;
+    int32_t* dcnt = dtok + rows * tokens_stride;
+    rc = cuda_check(cudaMemcpyAsync(c->ws_io, q_host, nq * 2, cudaMemcpyHostToDevice, st), "h2d q");
+    if (!rc) rc = cuda_check(cudaMemcpyAsync(dtok, tokens_host, rows * tokens_stride * 4, cudaMemcpyHostToDevice, st), "h2d tokens");
+    if (!rc) rc = cuda_check(cudaMemcpyAsync(dcnt, counts_host, rows * 4, cudaMemcpyHostToDevice, st), "h2d counts");
+    if (!rc)
+        rc = qk_attend_tokens(c, layer, c->ws_io, batch, dtok, tokens_stride, dcnt, c->ws_out,
+                              QK_DTYPE_F32, lse_host ? c->ws_lse : nullptr,
+                              wsum_host ? c->ws_wsum : nullptr, stream);
+    if (!rc) rc = copy_results(c, out_host, lse_host, wsum_host, rows, nq, st);
+    const int rs = cuda_check(cudaStreamSynchronize(st), "qk_attend_tokens_host");
+    cudaFree(dtok);
+    if (!rc) rc = rs;
+    if (!rc) rc = qk_check_status(c, stream);
+    return rc;
+}
+
+int qk_attention_logits_host(const qk_cache* cc, uint32_t layer, const uint16_t* q_host,
+                             uint32_t batch, const int32_t* tokens_host, uint32_t tokens_stride,
+                             const int32_t* counts_host, double* logits_host,
+                             uint32_t logits_stride, void* stream) {
+    qk_cache* c = const_cast<qk_cache*>(cc);
+    if (!c || !q_host || !logits_host || (tokens_host && !counts_host))
+        return set_error(QK_ERR_INVALID_ARGUMENT, "attention_logits: null argument");
+    if (int rc = check_layer_batch(c, layer, batch, "attention_logits")) return rc;
+    const size_t rows = size_t(batch) * c->Hq;
+    if (tokens_host) {
+        if (int rc = check_token_sets(c, layer, tokens_host, tokens_stride, counts_host, rows)) return rc;
+    } else {
+        for (uint32_t b = 0; b < batch; ++b) {
+            const uint32_t t = c->h_len[size_t(layer) * c->B + b];
+            if (t == 0) return set_error(QK_ERR_INVALID_ARGUMENT, "attention: empty token set");
+            if (t > logits_stride)
+                return set_error(QK_ERR_INVALID_ARGUMENT, "attention_logits: logits_stride below the token count");
+        }
+    }
+    if (tokens_host && logits_stride < tokens_stride)
+        return set_error(QK_ERR_INVALID_ARGUMENT, "attention_logits: logits_stride below the list");
+    DeviceGuard guard(c->desc.device);
+    cudaStream_t st = as_stream(stream);
+    const size_t nq = rows * c->desc.head_dim;
+    const size_t ntok = tokens_host ? rows * tokens_stride + rows : 0;
+    int32_t* dtok = nullptr;
+    double* dlog = nullptr;
+    int rc = cuda_check(cudaMalloc(&dlog, rows * logits_stride * sizeof(double) + ntok * 4), "attention_logits");
+    if (rc) return rc;
+    if (tokens_host) dtok = reinterpret_cast<int32_t*>(dlog + rows * logits_stride);
+    rc = cuda_check(cudaMemcpyAsync(c->ws_io, q_host, nq * 2, cudaMemcpyHostToDevice, st), "h2d q");
+    if (!rc && dtok)
+        rc = cuda_check(cudaMemcpyAsync(dtok, tokens_host, rows * tokens_stride * 4, cudaMemcpyHostToDevice, st), "h2d tokens");
+    if (!rc && dtok)
+        rc = cuda_check(cudaMemcpyAsync(dtok + rows * tokens_stride, counts_host, rows * 4, cudaMemcpyHostToDevice, st), "h2d counts");
+    if (!rc)
+        rc = qk_attention_logits(c, layer, c->ws_io, batch, dtok, tokens_stride,
+                                 dtok ? dtok + rows * tokens_stride : nullptr, dlog, logits_stride, stream);
+    if (!rc)
+        rc = cuda_check(cudaMemcpyAsync(logits_host, dlog, rows * logits_stride * sizeof(double),
+                                        cudaMemcpyDeviceToHost, st), "d2h logits");
+    const int rs = cuda_check(cudaStreamSynchronize(st), "qk_attention_logits_host");
+    cudaFree(dlog);
+    if (!rc) rc = rs;
+    if (!rc) rc = qk_check_status(c, stream);
+    return rc;
+}
+
+int qk_estimate_metadata_host(const uint16_t* q_host, const uint16_t* min_host,
+                              const uint16_t* max_host, uint32_t n_pages, uint32_t head_dim,
+                              double* scores_host, int32_t device) {
+    if (!q_host || (n_pages && (!min_host || !max_host || !scores_host)))
+        return set_error(QK_ERR_INVALID_ARGUMENT, "estimate_page_score: null argument");
+    if (head_dim == 0) return set_error(QK_ERR_INVALID_ARGUMENT, "estimate_page_score: dimension mismatch");
+    if (n_pages == 0) return QK_OK;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return set_error(QK_ERR_CUDA, "estimate_page_score: no CUDA device (this library has no CPU path)");
+    if (device < 0 || device >= ndev) return set_error(QK_ERR_INVALID_ARGUMENT, "estimate_page_score: bad device");
+    DeviceGuard guard(device);
+    // Per-device grow-only scratch (no allocation per call once warm).
+    static std::mutex mu;
+    static std::map<int, std::pair<void*, size_t>> scratch;
+    std::lock_guard<std::mutex> lock(mu);
+    const size_t halves = size_t(head_dim) * (1 + 2 * size_t(n_pages));
+    const size_t need = ((halves * 2 + 15) & ~size_t(15)) + size_t(n_pages) * 8;
+    auto& sl = scratch[device];
+    if (sl.second < need) {
+        if (sl.first) cudaFree(sl.first);
+        sl = {nullptr, 0};
+        void* p = nullptr;
+        if (int rc = cuda_check(cudaMalloc(&p, need), "estimate_page_score")) return rc;
+        sl = {p, need};
+    }
+    __half* dq = static_cast<__half*>(sl.first);
+    __half* dmn = dq + head_dim;
+    __half* dmx = dmn + size_t(n_pages) * head_dim;
+    double* dout = reinterpret_cast<double*>(static_cast<unsigned char*>(sl.first) +
+                                             ((halves * 2 + 15) & ~size_t(15)));
+    const size_t nb = size_t(n_pages) * head_dim * 2;
+    int rc = cuda_check(cudaMemcpy(dq, q_host, head_dim * 2, cudaMemcpyHostToDevice), "h2d q");
+    if (!rc) rc = cuda_check(cudaMemcpy(dmn, min_host, nb, cudaMemcpyHostToDevice), "h2d min");
+    if (!rc) rc = cuda_check(cudaMemcpy(dmx, max_host, nb, cudaMemcpyHostToDevice), "h2d max");
+    if (!rc) rc = launch_page_scores(dq, dmn, dmx, n_pages, head_dim, dout, nullptr);
+    if (!rc) rc = cuda_check(cudaMemcpy(scores_host, dout, size_t(n_pages) * 8, cudaMemcpyDeviceToHost), "d2h");
+    return rc;
+}
+
+int qk_softmax_weights_host(const double* logits_host, uint32_t n, double* weights_host,
+                            int32_t device) {
+    if (!logits_host || !weights_host)
+        return set_error(QK_ERR_INVALID_ARGUMENT, "softmax_weights: null argument");
+    if (n == 0) return set_error(QK_ERR_INVALID_ARGUMENT, "softmax_weights: empty logits");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return set_error(QK_ERR_CUDA, "softmax_weights: no CUDA device (this library has no CPU path)");
+    if (device < 0 || device >= ndev) return set_error(QK_ERR_INVALID_ARGUMENT, "softmax_weights: bad device");
+    DeviceGuard guard(device);
+    double* d = nullptr;
+    int rc = cuda_check(cudaMalloc(&d, size_t(n) * 2 * sizeof(double)), "softmax_weights");
+    if (rc) return rc;
+    rc = cuda_check(cudaMemcpy(d, logits_host, size_t(n) * 8, cudaMemcpyHostToDevice), "h2d logits");
+    if (!rc) rc = launch_softmax(d, nullptr, n, n, 1, d + n, nullptr, nullptr);
+    if (!rc) rc = cuda_check(cudaMemcpy(weights_host, d + n, size_t(n) * 8, cudaMemcpyDeviceToHost), "d2h weights");
+    cudaFree(d);
+    return rc;
+}
+
 int qk_dense_attend_host(const qk_cache* cc, uint32_t layer, const uint16_t* q_host,
-                         uint32_t batch, float* out_host, float* lse_host, void* stream) {
+                         uint32_t batch, float* out_host, float* lse_host, double* wsum_host,
+                         void* stream) {
     qk_cache* c = const_cast<qk_cache*>(cc);
     if (!c || !q_host || !out_host)
         return set_error(QK_ERR_INVALID_ARGUMENT, "full_attention: null argument");
@@ -732,10 +1031,10 @@ int qk_dense_attend_host(const qk_cache* cc, uint32_t layer, const uint16_t* q_h
     const size_t nq = rows * c->desc.head_dim;
     float* dlse = lse_host ? c->ws_lse : nullptr;
     int rc = cuda_check(cudaMemcpyAsync(c->ws_io, q_host, nq * 2, cudaMemcpyHostToDevice, st), "h2d q");
-    if (!rc) rc = qk_dense_attend(c, layer, c->ws_io, batch, c->ws_out, QK_DTYPE_F32, dlse, stream);
-    if (!rc) rc = cuda_check(cudaMemcpyAsync(out_host, c->ws_out, nq * 4, cudaMemcpyDeviceToHost, st), "d2h out");
-    if (!rc && lse_host)
-        rc = cuda_check(cudaMemcpyAsync(lse_host, dlse, rows * 4, cudaMemcpyDeviceToHost, st), "d2h lse");
+    if (!rc)
+        rc = qk_dense_attend(c, layer, c->ws_io, batch, c->ws_out, QK_DTYPE_F32, dlse,
+                             wsum_host ? c->ws_wsum : nullptr, stream);
+    if (!rc) rc = copy_results(c, out_host, lse_host, wsum_host, rows, nq, st);
     if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "qk_dense_attend_host");
     return rc;
 }
@@ -805,6 +1104,14 @@ int qk_check_status(qk_cache* c, void* stream) {
             return set_error(QK_ERR_INVALID_ARGUMENT, "sparse_attention: empty page selection");
         case QK_DEV_CAPACITY:
             return set_error(QK_ERR_OUT_OF_RANGE, "KvCache::append: cache slice is full");
+        case QK_DEV_TOKEN_OUT_OF_RANGE:
+            return set_error(QK_ERR_OUT_OF_RANGE, "attention: token index out of range");
+        case QK_DEV_TOKEN_NOT_ASCENDING:
+            return set_error(QK_ERR_INVALID_ARGUMENT, "attention: token set must be strictly ascending");
+        case QK_DEV_EMPTY_TOKENS:
+            return set_error(QK_ERR_INVALID_ARGUMENT, "attention: empty token set");
+        case QK_DEV_SCORE_PAGE_OUT_OF_RANGE:
+            return set_error(QK_ERR_OUT_OF_RANGE, "select_top_k: score for nonexistent page");
         case QK_DEV_BAD_COUNT:
             return set_error(QK_ERR_INVALID_ARGUMENT,
                              "sparse_attention: page count exceeds the page list (pages_stride)");

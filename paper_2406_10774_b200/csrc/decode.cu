@@ -1061,8 +1061,8 @@ int decode_unfused(qk_cache* c, uint32_t layer, const __half* q, const __half* k
     if (rc) return rc;
     const uint32_t kk = eff.token_budget / c->S;
     const uint32_t max_list = kk < c->Pmax ? kk : c->Pmax;
-    return launch_attend(c, layer, q, batch, sel, sstride, cnt, false, max_list, out, out_dtype,
-                         nullptr, st);
+    return launch_attend(c, layer, q, batch, sel, sstride, cnt, kModePages, max_list, out, out_dtype,
+                         nullptr, nullptr, st);
 }
 
 }  // namespace

@@ -76,6 +76,7 @@ struct qk_cache {
     uint16_t* ws_io = nullptr;           // staging for qk_decode_step_host
     float* ws_out = nullptr;             // [B][Hq][head_dim] fp32
     float* ws_lse = nullptr;             // [B][Hq] fp32 (host-buffer entry points)
+    double* ws_wsum = nullptr;           // [B][Hq] f64 weights_sum_check (host-buffer entry points)
     unsigned char* host_stage = nullptr; // pinned, device-mapped staging of the host step
     unsigned char* host_stage_dev = nullptr;  // (q, k, v in; fp32 out), allocated lazily
     // Host-step completion: the last unit of a fused launch writes `seq` into the mapped word
@@ -103,7 +104,14 @@ enum : int32_t {
     QK_DEV_EMPTY_SELECTION = 3,
     QK_DEV_CAPACITY = 4,
     QK_DEV_BAD_COUNT = 5,  // a page/token count past its list row or the launched splits
+    QK_DEV_TOKEN_OUT_OF_RANGE = 6,   // attend_tokens / attention_logits (check_token_set)
+    QK_DEV_TOKEN_NOT_ASCENDING = 7,
+    QK_DEV_EMPTY_TOKENS = 8,
+    QK_DEV_SCORE_PAGE_OUT_OF_RANGE = 9,  // select_top_k: score for a nonexistent page
 };
+
+// launch_attend list modes.
+enum : int { kModePages = 0, kModeDense = 1, kModeTokens = 2 };
 
 // Kernel launchers (one translation unit each).
 namespace qk {
@@ -118,8 +126,18 @@ int launch_topk(const qk_cache* c, uint32_t layer, const double* scores, uint32_
                 uint32_t pstride, int32_t* counts, uint32_t max_pages, cudaStream_t st);
 int launch_attend(const qk_cache* c, uint32_t layer, const __half* q, uint32_t batch,
                   const int32_t* pages, uint32_t pstride, const int32_t* counts,
-                  bool dense, uint32_t max_list, void* out, int out_dtype, float* lse,
-                  cudaStream_t st);
+                  int mode, uint32_t max_list, void* out, int out_dtype, float* lse,
+                  double* weights_sum, cudaStream_t st);
+int launch_topk_pairs(const qk_cache* c, uint32_t layer, uint32_t seq, const uint32_t* page_index,
+                      const double* score, uint32_t n, uint32_t k, int force, int all_pages,
+                      uint32_t capacity, int32_t* pages, int32_t* count, cudaStream_t st);
+int launch_logits(const qk_cache* c, uint32_t layer, const __half* q, uint32_t batch,
+                  const int32_t* tokens, uint32_t tstride, const int32_t* counts,
+                  uint32_t max_list, double* logits, uint32_t lstride, cudaStream_t st);
+int launch_page_scores(const __half* q, const __half* mn, const __half* mx, uint32_t n,
+                       uint32_t d, double* out, cudaStream_t st);
+int launch_softmax(const double* logits, const int32_t* counts, uint32_t n, uint32_t stride,
+                   uint32_t rows, double* weights, int32_t* status, cudaStream_t st);
 int launch_decode(qk_cache* c, uint32_t layer, const __half* q, const __half* k,
                   const __half* v, uint32_t batch, const qk_selection_cfg& cfg,
                   uint32_t max_pages_after, void* out, int out_dtype, int32_t* pages,

@@ -120,7 +120,10 @@ __device__ __forceinline__ int load_keys(const double* __restrict__ scores, uint
         for (int j = 0; j < 8; ++j) {
             const uint32_t i = uint32_t(t) * kpt + j0 + j;
             if (j0 + j < kpt && i < n) {
-                const unsigned long long u = order_key(v[j]);
+                // -0 and +0 compare equal in the reference's sort (criticality.cpp:64-67: ties
+                // go to the lower page): canonicalise before keying (user-supplied scores;
+                // estimate sums start at +0 and are never -0).
+                const unsigned long long u = order_key(__dadd_rn(v[j], 0.0));
                 keys[t * (kpt + 1) + j0 + j] = u;
                 kmax = u > kmax ? u : kmax;
                 kmin = u < kmin ? u : kmin;

@@ -44,6 +44,9 @@ __all__ = [
     "select_top_k",
     "sparse_attention",
     "full_attention",
+    "attend_tokens",
+    "attention_logits",
+    "softmax_weights",
     "traffic_fraction",
 ]
 
@@ -207,35 +210,111 @@ class QuestCache:
                                        _ptr(counts), _stream_ptr(stream)))
         return pages, counts
 
-    def sparse_attend(self, layer: int, q: torch.Tensor, pages: torch.Tensor, counts: torch.Tensor,
-                      out_dtype: torch.dtype = torch.float32, want_lse: bool = False,
-                      stream=None):
-        q = self._check_q(q)
-        batch = q.shape[0]
+    def _attn_outputs(self, batch, out_dtype, want_lse, want_wsum):
         out = torch.empty((batch, self.num_q_heads, self.head_dim), dtype=out_dtype,
                           device=self.device)
         lse = torch.empty((batch, self.num_q_heads), dtype=torch.float32,
                           device=self.device) if want_lse else None
+        wsum = torch.empty((batch, self.num_q_heads), dtype=torch.float64,
+                           device=self.device) if want_wsum else None
         dt = _lib.QK_DTYPE_F32 if out_dtype == torch.float32 else _lib.QK_DTYPE_F16
+        return out, lse, wsum, dt
+
+    @staticmethod
+    def _attn_result(out, lse, wsum):
+        res = (out,) + ((lse,) if lse is not None else ()) + ((wsum,) if wsum is not None else ())
+        return res[0] if len(res) == 1 else res
+
+    def sparse_attend(self, layer: int, q: torch.Tensor, pages: torch.Tensor, counts: torch.Tensor,
+                      out_dtype: torch.dtype = torch.float32, want_lse: bool = False,
+                      want_weights_sum: bool = False, stream=None):
+        """sparse_attention per (sequence, query head); returns out [, lse] [, weights_sum]."""
+        q = self._check_q(q)
+        batch = q.shape[0]
+        out, lse, wsum, dt = self._attn_outputs(batch, out_dtype, want_lse, want_weights_sum)
         pages = pages.to(torch.int32).contiguous()
         counts = counts.to(torch.int32).contiguous()
         check(self._lib.qk_sparse_attend(self._h, layer, _ptr(q), batch, _ptr(pages),
                                          pages.shape[-1], _ptr(counts), _ptr(out), dt, _ptr(lse),
-                                         _stream_ptr(stream)))
-        return (out, lse) if want_lse else out
+                                         _ptr(wsum), _stream_ptr(stream)))
+        return self._attn_result(out, lse, wsum)
 
     def dense_attend(self, layer: int, q: torch.Tensor, out_dtype: torch.dtype = torch.float32,
-                     want_lse: bool = False, stream=None):
+                     want_lse: bool = False, want_weights_sum: bool = False, stream=None):
+        """full_attention per (sequence, query head); returns out [, lse] [, weights_sum]."""
         q = self._check_q(q)
         batch = q.shape[0]
-        out = torch.empty((batch, self.num_q_heads, self.head_dim), dtype=out_dtype,
-                          device=self.device)
-        lse = torch.empty((batch, self.num_q_heads), dtype=torch.float32,
-                          device=self.device) if want_lse else None
-        dt = _lib.QK_DTYPE_F32 if out_dtype == torch.float32 else _lib.QK_DTYPE_F16
+        out, lse, wsum, dt = self._attn_outputs(batch, out_dtype, want_lse, want_weights_sum)
         check(self._lib.qk_dense_attend(self._h, layer, _ptr(q), batch, _ptr(out), dt, _ptr(lse),
-                                        _stream_ptr(stream)))
-        return (out, lse) if want_lse else out
+                                        _ptr(wsum), _stream_ptr(stream)))
+        return self._attn_result(out, lse, wsum)
+
+    def attend_tokens(self, layer: int, q: torch.Tensor, tokens: torch.Tensor,
+                      counts: torch.Tensor, out_dtype: torch.dtype = torch.float32,
+                      want_lse: bool = False, want_weights_sum: bool = False, stream=None):
+        """attend_tokens (attention.cpp:69-84) per (sequence, query head) over explicit,
+        strictly ascending token lists tokens [batch, Hq, stride] (counts [batch, Hq]);
+        invalid lists surface at check_status()."""
+        q = self._check_q(q)
+        batch = q.shape[0]
+        out, lse, wsum, dt = self._attn_outputs(batch, out_dtype, want_lse, want_weights_sum)
+        tokens = tokens.to(torch.int32).contiguous()
+        counts = counts.to(torch.int32).contiguous()
+        check(self._lib.qk_attend_tokens(self._h, layer, _ptr(q), batch, _ptr(tokens),
+                                         tokens.shape[-1], _ptr(counts), _ptr(out), dt, _ptr(lse),
+                                         _ptr(wsum), _stream_ptr(stream)))
+        return self._attn_result(out, lse, wsum)
+
+    def attention_logits(self, layer: int, q: torch.Tensor, tokens: Optional[torch.Tensor] = None,
+                         counts: Optional[torch.Tensor] = None, stride: Optional[int] = None,
+                         stream=None) -> torch.Tensor:
+        """attention_logits (attention.cpp:34-52): f64 [batch, Hq, stride], bitwise the
+        reference's; tokens None -> every cached token (stride defaults to max_tokens)."""
+        q = self._check_q(q)
+        batch = q.shape[0]
+        if tokens is not None:
+            tokens = tokens.to(torch.int32).contiguous()
+            counts = counts.to(torch.int32).contiguous()
+            stride = tokens.shape[-1] if stride is None else stride
+        elif stride is None:
+            stride = self.max_tokens
+        logits = torch.zeros((batch, self.num_q_heads, stride), dtype=torch.float64,
+                             device=self.device)
+        check(self._lib.qk_attention_logits(self._h, layer, _ptr(q), batch, _ptr(tokens),
+                                            0 if tokens is None else tokens.shape[-1],
+                                            _ptr(counts), _ptr(logits), stride,
+                                            _stream_ptr(stream)))
+        return logits
+
+    def softmax_weights(self, logits: torch.Tensor, counts: Optional[torch.Tensor] = None,
+                        stream=None) -> torch.Tensor:
+        """softmax_weights (attention.cpp:54-67) over the rows of f64 logits [..., stride]
+        (counts: valid entries per row; None = the whole row)."""
+        lg = logits.to(torch.float64).contiguous()
+        stride = lg.shape[-1]
+        rows = lg.numel() // max(stride, 1)
+        if counts is not None:
+            counts = counts.to(torch.int32).contiguous()
+        w = torch.zeros_like(lg)
+        check(self._lib.qk_softmax_weights(self._h, _ptr(lg), _ptr(counts), stride, stride, rows,
+                                           _ptr(w), _stream_ptr(stream)))
+        return w
+
+    def select_topk_pairs(self, layer: int, seq: int, page_index: torch.Tensor,
+                          scores: torch.Tensor, token_budget: int, force_include_recent: bool = True,
+                          per_layer_enabled: bool = True, stream=None):
+        """select_top_k on an arbitrary PageScore vector (any order, repeats allowed):
+        returns (pages int32 [capacity], count int32 [1])."""
+        pi = page_index.to(torch.int32).contiguous()
+        sc = scores.to(torch.float64).contiguous()
+        cap = max(self.max_pages, token_budget // self.page_size, 1)
+        pages = torch.full((cap,), -1, dtype=torch.int32, device=self.device)
+        count = torch.zeros((1,), dtype=torch.int32, device=self.device)
+        cfg = _sel_cfg(token_budget, force_include_recent, per_layer_enabled)
+        check(self._lib.qk_select_topk_pairs(self._h, layer, seq, _ptr(pi), _ptr(sc), pi.numel(),
+                                             ctypes.byref(cfg), _ptr(pages), cap, _ptr(count),
+                                             _stream_ptr(stream)))
+        return pages, count
 
     def decode_step(self, layer: int, q: torch.Tensor, k: Optional[torch.Tensor],
                     v: Optional[torch.Tensor], token_budget: int, force_include_recent: bool = True,
@@ -455,11 +534,11 @@ class SelectionConfig:
 
 @dataclass
 class AttentionOutput:
-    """attention.hpp:15-18.  weights_sum_check is 1 by construction: the kernel divides
-    by the merged softmax normaliser."""
+    """attention.hpp:15-18.  weights_sum_check: the post-softmax mass of the weights the
+    kernel applied (fp64 from its fp32 partials; 1 up to fp32 rounding of the normaliser)."""
 
     output: List[float]
-    weights_sum_check: float = 1.0
+    weights_sum_check: float = 0.0
 
 
 def _query_dev(query, cache: KvCache) -> torch.Tensor:
@@ -495,8 +574,9 @@ def estimate_page_score(query, metadata: PageMetadata) -> float:
 
 def select_top_k(scores: Sequence[PageScore], config: SelectionConfig,
                  cache: KvCache) -> List[int]:
-    """criticality.cpp:36-81 on the GPU top-K kernel.  Scores must be estimate_all's form
-    (one per page, in page order)."""
+    """criticality.cpp:36-81 on the GPU.  estimate_all's form (one score per page, in page
+    order) takes the radix top-K kernel; any other PageScore vector (any order, repeated
+    pages) takes the pair-sorting kernel, with the reference's exact semantics."""
     P = cache.page_count()
     if not config.per_layer_enabled:
         return list(range(P))
@@ -507,14 +587,23 @@ def select_top_k(scores: Sequence[PageScore], config: SelectionConfig,
     for s in scores:
         if s.page_index >= P:
             raise IndexError("select_top_k: score for nonexistent page")
-    if [s.page_index for s in scores] != list(range(P)):
-        raise ValueError("select_top_k: the GPU selector takes one score per page in page order")
     qc = cache.quest_cache
-    dev = torch.tensor([s.score for s in scores], dtype=torch.float64, device=qc.device)
-    pages, counts = qc.select_topk(0, dev.view(1, 1, -1), config.token_budget,
-                                   config.force_include_recent, config.per_layer_enabled)
-    n = int(counts[0, 0])
-    return pages[0, 0, :n].cpu().tolist()
+    if [s.page_index for s in scores] == list(range(P)):
+        dev = torch.tensor([s.score for s in scores], dtype=torch.float64, device=qc.device)
+        pages, counts = qc.select_topk(0, dev.view(1, 1, -1), config.token_budget,
+                                       config.force_include_recent, config.per_layer_enabled)
+        n = int(counts[0, 0])
+        return pages[0, 0, :n].cpu().tolist()
+    pi = np.array([s.page_index for s in scores], dtype=np.uint32)
+    sc = np.array([s.score for s in scores], dtype=np.float64)
+    cap = max(P, config.token_budget // cache.config().page_size, 1)
+    out = np.zeros(cap, dtype=np.int32)
+    cnt = ctypes.c_int32()
+    cfg = _sel_cfg(config.token_budget, config.force_include_recent, config.per_layer_enabled)
+    check(qc._lib.qk_select_topk_pairs_host(qc._h, 0, 0, pi.ctypes.data, sc.ctypes.data, len(pi),
+                                            ctypes.byref(cfg), out.ctypes.data, cap,
+                                            ctypes.byref(cnt), None))
+    return out[: cnt.value].tolist()
 
 
 def sparse_attention(query, cache: KvCache, selected_pages: Sequence[int]) -> AttentionOutput:
@@ -532,17 +621,75 @@ def sparse_attention(query, cache: KvCache, selected_pages: Sequence[int]) -> At
     qc = cache.quest_cache
     pl = torch.tensor(pages, dtype=torch.int32, device=qc.device).view(1, 1, -1)
     cnt = torch.tensor([[len(pages)]], dtype=torch.int32, device=qc.device)
-    out = qc.sparse_attend(0, _query_dev(query, cache), pl, cnt)
+    out, ws = qc.sparse_attend(0, _query_dev(query, cache), pl, cnt, want_weights_sum=True)
     qc.check_status()
-    return AttentionOutput(out[0, 0].double().cpu().tolist())
+    return AttentionOutput(out[0, 0].double().cpu().tolist(), float(ws[0, 0]))
 
 
 def full_attention(query, cache: KvCache) -> AttentionOutput:
     """attention.cpp:86-92 (empty cache -> ValueError)."""
     if cache.token_count() == 0:
         raise ValueError("full_attention: empty cache")
-    out = cache.quest_cache.dense_attend(0, _query_dev(query, cache))
-    return AttentionOutput(out[0, 0].double().cpu().tolist())
+    out, ws = cache.quest_cache.dense_attend(0, _query_dev(query, cache), want_weights_sum=True)
+    return AttentionOutput(out[0, 0].double().cpu().tolist(), float(ws[0, 0]))
+
+
+def _check_token_set(cache: KvCache, tokens: Sequence[int]) -> List[int]:
+    """check_token_set (attention.cpp:19-30), same errors (ValueError / IndexError)."""
+    toks = [int(t) for t in tokens]
+    if not toks:
+        raise ValueError("attention: empty token set")
+    n = cache.token_count()
+    for i, t in enumerate(toks):
+        if t < 0 or t >= n:
+            raise IndexError("attention: token index out of range")
+        if i > 0 and t <= toks[i - 1]:
+            raise ValueError("attention: token set must be strictly ascending")
+    return toks
+
+
+def attend_tokens(query, cache: KvCache, tokens: Sequence[int]) -> AttentionOutput:
+    """attention.cpp:69-84: attention over an explicit strictly ascending token set."""
+    toks = _check_token_set(cache, tokens)
+    if len(np.asarray(query).reshape(-1)) != cache.config().head_dim:
+        raise ValueError("attention_logits: query dimension mismatch")
+    qc = cache.quest_cache
+    tl = torch.tensor(toks, dtype=torch.int32, device=qc.device).view(1, 1, -1)
+    cnt = torch.tensor([[len(toks)]], dtype=torch.int32, device=qc.device)
+    out, ws = qc.attend_tokens(0, _query_dev(query, cache), tl, cnt, want_weights_sum=True)
+    qc.check_status()
+    return AttentionOutput(out[0, 0].double().cpu().tolist(), float(ws[0, 0]))
+
+
+def attention_logits(query, cache: KvCache, token_subset: Optional[Sequence[int]] = None):
+    """attention.cpp:34-52 (both overloads): logits q.k/sqrt(d) in ascending token order,
+    bitwise the reference's doubles."""
+    if token_subset is None:
+        toks = list(range(cache.token_count()))
+        if not toks:
+            raise ValueError("attention: empty token set")
+    else:
+        toks = _check_token_set(cache, token_subset)
+    if len(np.asarray(query).reshape(-1)) != cache.config().head_dim:
+        raise ValueError("attention_logits: query dimension mismatch")
+    qc = cache.quest_cache
+    tl = torch.tensor(toks, dtype=torch.int32, device=qc.device).view(1, 1, -1)
+    cnt = torch.tensor([[len(toks)]], dtype=torch.int32, device=qc.device)
+    lg = qc.attention_logits(0, _query_dev(query, cache), tl, cnt)
+    qc.check_status()
+    return lg[0, 0, : len(toks)].cpu().tolist()
+
+
+def softmax_weights(logits: Sequence[float], device: Optional[int] = None) -> List[float]:
+    """attention.cpp:54-67 on the GPU (empty -> ValueError)."""
+    lg = np.ascontiguousarray(np.asarray(logits, dtype=np.float64).reshape(-1))
+    if lg.size == 0:
+        raise ValueError("softmax_weights: empty logits")
+    w = np.empty_like(lg)
+    lib = _lib.load()
+    dev = torch.cuda.current_device() if device is None else device
+    check(lib.qk_softmax_weights_host(lg.ctypes.data, lg.size, w.ctypes.data, dev))
+    return w.tolist()
 
 
 def traffic_fraction(page_size: int, token_count: int, token_budget: int) -> float:

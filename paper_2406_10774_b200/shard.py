@@ -77,10 +77,14 @@ def gather_outputs(local_out: torch.Tensor, shards: Sequence[Shard], batch: int,
     if world != len(shards):
         raise ValueError("gather_outputs: one shard per rank expected")
     d = local_out.shape[-1]
-    parts = [torch.empty((s.num_requests, s.num_kv_heads * group_size, d), dtype=local_out.dtype,
-                         device=local_out.device) for s in shards]
+    # gloo has no CUDA all_gather: stage through host memory (tests, CPU-only rigs); NCCL
+    # gathers device tensors directly over NVLink.
+    via_host = local_out.is_cuda and dist.get_backend(process_group) == "gloo"
+    src = local_out.cpu() if via_host else local_out
+    parts = [torch.empty((s.num_requests, s.num_kv_heads * group_size, d), dtype=src.dtype,
+                         device=src.device) for s in shards]
     # all_gather needs equal shapes: every shard of a partition has the same rectangle size.
-    dist.all_gather(parts, local_out.contiguous(), group=process_group)
+    dist.all_gather(parts, src.contiguous(), group=process_group)
     full = torch.empty((batch, num_kv_heads * group_size, d), dtype=local_out.dtype,
                        device=local_out.device)
     for s, part in zip(shards, parts):
@@ -117,10 +121,31 @@ class ShardedDecoder:
                                 num_kv_heads=self.shard.num_kv_heads, max_tokens=max_tokens,
                                 device=device)
 
+    def local_q(self, q_full: torch.Tensor) -> torch.Tensor:
+        """This rank's slice [local_batch, local_Hq, d] of a full [batch, Hq, d] query."""
+        s = self.shard
+        return q_full[s.b0:s.b1, s.h0 * self.G:s.h1 * self.G].contiguous()
+
+    def local_kv(self, x_full: torch.Tensor) -> torch.Tensor:
+        """This rank's slice [local_batch, local_Hkv, ...] of a full [batch, Hkv, ...] tensor."""
+        s = self.shard
+        return x_full[s.b0:s.b1, s.h0:s.h1].contiguous()
+
+    def prefill(self, layer: int, seq: int, k_full: torch.Tensor, v_full: torch.Tensor,
+                stream=None) -> None:
+        """Bulk prefill of global sequence `seq` from all-head [Hkv, n, d] K/V (a no-op on
+        ranks that do not own it)."""
+        s = self.shard
+        if s.b0 <= seq < s.b1:
+            self.cache.prefill(layer, seq - s.b0, k_full[s.h0:s.h1].contiguous(),
+                               v_full[s.h0:s.h1].contiguous(), stream=stream)
+
     def decode_step(self, layer: int, q: torch.Tensor, k: Optional[torch.Tensor],
                     v: Optional[torch.Tensor], token_budget: int, gather: bool = True,
+                    force_include_recent: bool = True, per_layer_enabled: bool = True,
                     stream=None) -> torch.Tensor:
-        out = self.cache.decode_step(layer, q, k, v, token_budget, stream=stream)
+        out = self.cache.decode_step(layer, q, k, v, token_budget, force_include_recent,
+                                     per_layer_enabled, stream=stream)
         if not gather or len(self.shards) == 1:
             return out
         return gather_outputs(out, self.shards, self.batch, self.num_kv_heads, self.G, self.group)

@@ -21,7 +21,8 @@ def test_header_declares_the_operator_surface():
     syms = declared_symbols()
     for must in ("qk_cache_create", "qk_append", "qk_prefill", "qk_read_metadata", "qk_estimate",
                  "qk_select_topk", "qk_sparse_attend", "qk_dense_attend", "qk_decode_step",
-                 "qk_last_error"):
+                 "qk_attend_tokens", "qk_attention_logits", "qk_softmax_weights",
+                 "qk_select_topk_pairs", "qk_last_error"):
         assert must in syms
 
 
@@ -32,7 +33,7 @@ def test_library_exports_every_declared_symbol():
     for name in declared_symbols():
         assert hasattr(lib, name), name
         assert name in _lib.SIGNATURES, f"{name} lacks a ctypes signature"
-    assert lib.qk_abi_version() == 1
+    assert lib.qk_abi_version() == 2
 
 
 def test_library_is_sm100a_only():
