@@ -294,6 +294,41 @@ QK_API int qk_estimate_metadata_host(const uint16_t *q_host, const uint16_t *min
 QK_API int qk_softmax_weights_host(const double *logits_host, uint32_t n, double *weights_host,
                                    int32_t device);
 
+/* ---- GQA group-shared selection -------------------------------
+ * An OPT-IN variant, NOT the reference's semantics (the reference selects per query head,
+ * criticality.cpp:36-81): ONE page set per (sequence, KV head), chosen by select_top_k's
+ * rule (early exits, (score desc, page asc), force_include_recent) from a group score
+ * that combines the G exact per-query-head estimates of a page:
+ *   QK_GROUP_MAX  max over the group's query heads (exact, order-free)
+ *   QK_GROUP_SUM  fp64 sum in query-head order ((s_0 + s_1) + s_2) + ...
+ * Every query head of the group then attends over the shared pages (sparse_attention,
+ * attention.cpp:94-116, fp32 accumulate); K/V pages are read once per group and the
+ * Q.K^T / P.V contractions run on the tensor cores (mma.sync m16n8k16, G <= 8 heads,
+ * head_dim <= 128).  Group page lists / counts are [batch][num_kv_heads][stride] /
+ * [batch][num_kv_heads]; everything else as the per-head entry points. */
+enum qk_group_reduce { QK_GROUP_MAX = 1, QK_GROUP_SUM = 2 };
+
+/* select_top_k over the group scores of estimate_all's per-head scores (layout of
+ * qk_estimate's output). */
+QK_API int qk_select_topk_grouped(const qk_cache *cache, uint32_t layer, const double *scores,
+                                  uint32_t scores_stride, uint32_t batch,
+                                  const qk_selection_cfg *cfg, int32_t group_reduce,
+                                  int32_t *pages, uint32_t pages_stride, int32_t *counts,
+                                  void *stream);
+/* Every query head of a group attends over its group's page list (strictly ascending, in
+ * range; violations reported by qk_check_status as for qk_sparse_attend). */
+QK_API int qk_sparse_attend_grouped(const qk_cache *cache, uint32_t layer, const uint16_t *q,
+                                    uint32_t batch, const int32_t *pages, uint32_t pages_stride,
+                                    const int32_t *counts, void *out, int32_t out_dtype,
+                                    void *stream);
+/* append (optional) -> qk_estimate -> qk_select_topk_grouped -> qk_sparse_attend_grouped on
+ * `stream` (capturable in a CUDA graph). */
+QK_API int qk_decode_step_grouped(qk_cache *cache, uint32_t layer, const uint16_t *q,
+                                  const uint16_t *k, const uint16_t *v, uint32_t batch,
+                                  const qk_selection_cfg *cfg, int32_t group_reduce, void *out,
+                                  int32_t out_dtype, int32_t *pages_out, uint32_t pages_stride,
+                                  int32_t *counts_out, void *stream);
+
 /* Diagnostics / parity: with `on`, qk_decode_step estimates every page (also the forced
  * newest page, and when the budget covers the cache) and keeps the scores for
  * qk_debug_step_scores.  Off by default: the fused step then skips scores selection

@@ -143,6 +143,26 @@ class Oracle:
         out = self.sparse_attention(q, k, values, page_size, pages)
         return scores, pages, out
 
+    def group_quest_step(self, qs, keys, values, page_size: int, budget: int,
+                         reduce: str = "max", force: bool = True, enabled: bool = True):
+        """Checker of the GQA group-shared variant (not a reference
+        function -- composed from the restated ones): per query head g, estimate_all
+        (criticality.cpp:25-34) on the shared KV head's metadata; the group score of a page
+        is max_g (exact) or the fp64 sum in head order ((s_0 + s_1) + s_2) + ...; ONE
+        select_top_k (criticality.cpp:36-81) on the group scores; every head's
+        sparse_attention (attention.cpp:94-116) over that page set.
+        Returns (group_scores, pages, outputs [G][d])."""
+        qs = _f32(qs)
+        k = _f32(keys)
+        mn, mx = self.metadata(k, page_size)
+        per_head = [self.estimate_all(q, mn, mx) for q in qs]
+        group = per_head[0].copy()
+        for s in per_head[1:]:
+            group = np.maximum(group, s) if reduce == "max" else group + s  # IEEE fp64 adds
+        pages = self.select_top_k(group, page_size, budget, force, enabled)
+        outs = np.stack([self.sparse_attention(q, k, values, page_size, pages) for q in qs])
+        return group, pages, outs
+
     def traffic_fraction(self, page_size, token_count, budget) -> float:
         return float(self.lib.qo_traffic_fraction(page_size, token_count, budget))
 

@@ -25,6 +25,9 @@ QK_ERR_UNSUPPORTED = 4
 QK_DTYPE_F32 = 0
 QK_DTYPE_F16 = 1
 
+QK_GROUP_MAX = 1
+QK_GROUP_SUM = 2
+
 
 class qk_cache_desc(ctypes.Structure):
     _fields_ = [
@@ -110,6 +113,16 @@ SIGNATURES = {
     "qk_attention_logits_host": (ctypes.c_int, [_P, _U32, _P, _U32, _P, _U32, _P, _P, _U32, _P]),
     "qk_softmax_weights_host": (ctypes.c_int, [_P, _U32, _P, _I32]),
     "qk_estimate_metadata_host": (ctypes.c_int, [_P, _P, _P, _U32, _U32, _P, _I32]),
+    "qk_select_topk_grouped": (
+        ctypes.c_int,
+        [_P, _U32, _P, _U32, _U32, ctypes.POINTER(qk_selection_cfg), _I32, _P, _U32, _P, _P],
+    ),
+    "qk_sparse_attend_grouped": (ctypes.c_int, [_P, _U32, _P, _U32, _P, _U32, _P, _P, _I32, _P]),
+    "qk_decode_step_grouped": (
+        ctypes.c_int,
+        [_P, _U32, _P, _P, _P, _U32, ctypes.POINTER(qk_selection_cfg), _I32, _P, _I32, _P, _U32,
+         _P, _P],
+    ),
 }
 
 _lib = None

@@ -656,6 +656,100 @@ int qk_decode_step(qk_cache* c, uint32_t layer, const uint16_t* q, const uint16_
     return QK_OK;
 }
 
+int qk_select_topk_grouped(const qk_cache* c, uint32_t layer, const double* scores,
+                           uint32_t scores_stride, uint32_t batch, const qk_selection_cfg* cfg,
+                           int32_t group_reduce, int32_t* pages, uint32_t pages_stride,
+                           int32_t* counts, void* stream) {
+    if (!c || !scores || !cfg || !pages || !counts)
+        return set_error(QK_ERR_INVALID_ARGUMENT, "select_top_k: null argument");
+    if (int rc = check_layer_batch(c, layer, batch, "select_top_k")) return rc;
+    if (group_reduce != QK_GROUP_MAX && group_reduce != QK_GROUP_SUM)
+        return set_error(QK_ERR_INVALID_ARGUMENT, "select_top_k: bad group_reduce");
+    bool empty = false;
+    const uint32_t mp = max_pages(c, layer, batch, &empty);
+    uint32_t kk = UINT32_MAX;  // every page (criticality.cpp:47)
+    if (cfg->per_layer_enabled) {
+        if (cfg->token_budget < c->S)
+            return set_error(QK_ERR_INVALID_ARGUMENT, "select_top_k: token_budget below page_size");
+        if (empty) return set_error(QK_ERR_INVALID_ARGUMENT, "select_top_k: no scores");
+        kk = cfg->token_budget / c->S;
+    }
+    const uint32_t need = kk < mp ? kk : mp;
+    if (pages_stride < need)
+        return set_error(QK_ERR_INVALID_ARGUMENT, "select_top_k: pages_stride below selection size");
+    if (scores_stride < mp)
+        return set_error(QK_ERR_INVALID_ARGUMENT, "select_top_k: scores_stride below page count");
+    if (c->G > 8 || (c->G & (c->G - 1)))
+        return set_error(QK_ERR_UNSUPPORTED, "grouped decode: GQA group must be 1, 2, 4 or 8");
+    DeviceGuard guard(c->desc.device);
+    return launch_group_topk(c, layer, scores, scores_stride, batch, kk,
+                             cfg->force_include_recent ? 1 : 0, group_reduce, pages,
+                             pages_stride, counts, as_stream(stream));
+}
+
+int qk_sparse_attend_grouped(const qk_cache* c, uint32_t layer, const uint16_t* q, uint32_t batch,
+                             const int32_t* pages, uint32_t pages_stride, const int32_t* counts,
+                             void* out, int32_t out_dtype, void* stream) {
+    if (!c || !q || !pages || !counts || !out)
+        return set_error(QK_ERR_INVALID_ARGUMENT, "sparse_attention: null argument");
+    if (int rc = check_layer_batch(c, layer, batch, "sparse_attention")) return rc;
+    if (out_dtype != QK_DTYPE_F32 && out_dtype != QK_DTYPE_F16)
+        return set_error(QK_ERR_INVALID_ARGUMENT, "sparse_attention: bad out_dtype");
+    if (pages_stride == 0)
+        return set_error(QK_ERR_INVALID_ARGUMENT, "sparse_attention: pages_stride is 0");
+    DeviceGuard guard(c->desc.device);
+    const uint32_t max_list = pages_stride < c->Pmax ? pages_stride : c->Pmax;
+    return launch_group_attend(c, layer, reinterpret_cast<const __half*>(q), batch, pages,
+                               pages_stride, counts, max_list, out, out_dtype, as_stream(stream));
+}
+
+int qk_decode_step_grouped(qk_cache* c, uint32_t layer, const uint16_t* q, const uint16_t* k,
+                           const uint16_t* v, uint32_t batch, const qk_selection_cfg* cfg,
+                           int32_t group_reduce, void* out, int32_t out_dtype, int32_t* pages_out,
+                           uint32_t pages_stride, int32_t* counts_out, void* stream) {
+    if (!c || !q || !cfg || !out)
+        return set_error(QK_ERR_INVALID_ARGUMENT, "qk_decode_step_grouped: null argument");
+    if (int rc = check_layer_batch(c, layer, batch, "qk_decode_step_grouped")) return rc;
+    if ((k == nullptr) != (v == nullptr))
+        return set_error(QK_ERR_INVALID_ARGUMENT, "qk_decode_step_grouped: k and v must both be given");
+    if (out_dtype != QK_DTYPE_F32 && out_dtype != QK_DTYPE_F16)
+        return set_error(QK_ERR_INVALID_ARGUMENT, "qk_decode_step_grouped: bad out_dtype");
+    if (group_reduce != QK_GROUP_MAX && group_reduce != QK_GROUP_SUM)
+        return set_error(QK_ERR_INVALID_ARGUMENT, "qk_decode_step_grouped: bad group_reduce");
+    if (cfg->per_layer_enabled && cfg->token_budget < c->S)
+        return set_error(QK_ERR_INVALID_ARGUMENT, "select_top_k: token_budget below page_size");
+    if (c->G > 8 || (c->G & (c->G - 1)) || c->D > 128)
+        return set_error(QK_ERR_UNSUPPORTED,
+                         "grouped decode: GQA group must be 1, 2, 4 or 8 and head_dim <= 128");
+    const uint32_t add = k ? 1 : 0;
+    uint32_t mp = 0;
+    for (uint32_t b = 0; b < batch; ++b) {
+        const uint32_t t = c->h_len[size_t(layer) * c->B + b];
+        if (t + add > c->desc.max_tokens)
+            return set_error(QK_ERR_OUT_OF_RANGE, "KvCache::append: cache slice is full");
+        if (t + add == 0) return set_error(QK_ERR_INVALID_ARGUMENT, "estimate_all: empty cache");
+        const uint32_t p = pages_of(c, t + add);
+        mp = p > mp ? p : mp;
+    }
+    const uint32_t kk = cfg->per_layer_enabled ? cfg->token_budget / c->S : UINT32_MAX;
+    const uint32_t need = kk < mp ? kk : mp;
+    if (pages_out) {
+        if (pages_stride < need || (kk >= c->Pmax && pages_stride < c->Pmax))
+            return set_error(QK_ERR_INVALID_ARGUMENT,
+                             "qk_decode_step_grouped: pages_stride below selection size");
+    }
+    DeviceGuard guard(c->desc.device);
+    const int rc = launch_decode_grouped(c, layer, reinterpret_cast<const __half*>(q),
+                                         reinterpret_cast<const __half*>(k),
+                                         reinterpret_cast<const __half*>(v), batch, *cfg,
+                                         group_reduce, mp, out, out_dtype, pages_out, pages_stride,
+                                         counts_out, as_stream(stream));
+    if (rc) return rc;
+    if (add)
+        for (uint32_t b = 0; b < batch; ++b) c->h_len[size_t(layer) * c->B + b] += 1;
+    return QK_OK;
+}
+
 int qk_decode_step_host(qk_cache* c, uint32_t layer, const uint16_t* q_host,
                         const uint16_t* k_host, const uint16_t* v_host, uint32_t batch,
                         const qk_selection_cfg* cfg, float* out_host, void* stream) {

@@ -138,6 +138,16 @@ int launch_page_scores(const __half* q, const __half* mn, const __half* mx, uint
                        uint32_t d, double* out, cudaStream_t st);
 int launch_softmax(const double* logits, const int32_t* counts, uint32_t n, uint32_t stride,
                    uint32_t rows, double* weights, int32_t* status, cudaStream_t st);
+int launch_group_topk(const qk_cache* c, uint32_t layer, const double* scores, uint32_t sstride,
+                      uint32_t batch, uint32_t k_budget, int force, int reduce, int32_t* pages,
+                      uint32_t pstride, int32_t* counts, cudaStream_t st);
+int launch_group_attend(const qk_cache* c, uint32_t layer, const __half* q, uint32_t batch,
+                        const int32_t* pages, uint32_t pstride, const int32_t* counts,
+                        uint32_t max_list, void* out, int out_dtype, cudaStream_t st);
+int launch_decode_grouped(qk_cache* c, uint32_t layer, const __half* q, const __half* k,
+                          const __half* v, uint32_t batch, const qk_selection_cfg& cfg,
+                          int reduce, uint32_t max_pages_after, void* out, int out_dtype,
+                          int32_t* pages, uint32_t pstride, int32_t* counts, cudaStream_t st);
 int launch_decode(qk_cache* c, uint32_t layer, const __half* q, const __half* k,
                   const __half* v, uint32_t batch, const qk_selection_cfg& cfg,
                   uint32_t max_pages_after, void* out, int out_dtype, int32_t* pages,

@@ -97,13 +97,13 @@ __device__ __forceinline__ unsigned long long keyat(const unsigned long long* ke
     return keys[(i / kpt) * (kpt + 1) + (i % kpt)];
 }
 
-// Loads scores[0..n) (global, written earlier in the same kernel or by a prior one) as
-// keys into `keys` (padded layout, capacity NT*(kpt+1)).  Returns kpt.
-template <int NT>
-__device__ __forceinline__ int load_keys(const double* __restrict__ scores, uint32_t n,
-                                         unsigned long long* keys, SelectScratch<NT>& sc,
-                                         unsigned long long* kmax_out,
-                                         unsigned long long* kmin_out) {
+// Loads score(0..n) -- `score(i)` returns candidate i's double (global data written
+// earlier in the same kernel or by a prior one) -- as keys into `keys` (padded layout,
+// capacity NT*(kpt+1)).  Returns kpt.
+template <int NT, typename ScoreFn>
+__device__ __forceinline__ int load_keys_fn(ScoreFn score, uint32_t n, unsigned long long* keys,
+                                            SelectScratch<NT>& sc, unsigned long long* kmax_out,
+                                            unsigned long long* kmin_out) {
     const int kpt = int((n + NT - 1) / NT);
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     unsigned long long kmax = 0, kmin = ~0ull;
@@ -114,7 +114,7 @@ __device__ __forceinline__ int load_keys(const double* __restrict__ scores, uint
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             const uint32_t i = uint32_t(t) * kpt + j0 + j;
-            v[j] = (j0 + j < kpt && i < n) ? __ldcg(scores + i) : 0.0;
+            v[j] = (j0 + j < kpt && i < n) ? score(i) : 0.0;
         }
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
@@ -152,6 +152,16 @@ __device__ __forceinline__ int load_keys(const double* __restrict__ scores, uint
     *kmax_out = kmax;
     *kmin_out = kmin;
     return kpt;
+}
+
+// load_keys_fn over one score row: scores[0..n).
+template <int NT>
+__device__ __forceinline__ int load_keys(const double* __restrict__ scores, uint32_t n,
+                                         unsigned long long* keys, SelectScratch<NT>& sc,
+                                         unsigned long long* kmax_out,
+                                         unsigned long long* kmin_out) {
+    return load_keys_fn<NT>([scores](uint32_t i) { return __ldcg(scores + i); }, n, keys, sc,
+                            kmax_out, kmin_out);
 }
 
 // Selects the `target` (1 <= target < n) best keys and writes their page indices,

@@ -338,6 +338,80 @@ class QuestCache:
                                        _stream_ptr(stream)))
         return out
 
+    # -- GQA group-shared selection (opt-in, not the reference's
+    #    per-head semantics -- see include/questkv_b200.h) ----------------------------------
+    _GROUP_REDUCE = {"max": _lib.QK_GROUP_MAX, "sum": _lib.QK_GROUP_SUM}
+
+    def _group_reduce(self, reduce: str) -> int:
+        if reduce not in self._GROUP_REDUCE:
+            raise ValueError("group_reduce must be 'max' or 'sum'")
+        return self._GROUP_REDUCE[reduce]
+
+    def _group_lists(self, batch, token_budget, per_layer_enabled, pages, counts):
+        if pages is None:
+            stride = self.max_pages
+            if per_layer_enabled and token_budget >= self.page_size:
+                stride = min(self.max_pages, token_budget // self.page_size)
+            pages = torch.full((batch, self.num_kv_heads, max(stride, 1)), -1, dtype=torch.int32,
+                               device=self.device)
+        if counts is None:
+            counts = torch.zeros((batch, self.num_kv_heads), dtype=torch.int32, device=self.device)
+        return pages, counts
+
+    def select_topk_grouped(self, layer: int, scores: torch.Tensor, token_budget: int,
+                            group_reduce: str = "max", force_include_recent: bool = True,
+                            per_layer_enabled: bool = True, pages: Optional[torch.Tensor] = None,
+                            counts: Optional[torch.Tensor] = None, stream=None):
+        """One page set per (sequence, KV head) from the group scores of estimate()'s per-head
+        scores: (pages int32 [batch, Hkv, stride], counts [batch, Hkv])."""
+        batch = scores.shape[0]
+        pages, counts = self._group_lists(batch, token_budget, per_layer_enabled, pages, counts)
+        cfg = _sel_cfg(token_budget, force_include_recent, per_layer_enabled)
+        check(self._lib.qk_select_topk_grouped(
+            self._h, layer, _ptr(scores), scores.shape[-1], batch, ctypes.byref(cfg),
+            self._group_reduce(group_reduce), _ptr(pages), pages.shape[-1], _ptr(counts),
+            _stream_ptr(stream)))
+        return pages, counts
+
+    def sparse_attend_grouped(self, layer: int, q: torch.Tensor, pages: torch.Tensor,
+                              counts: torch.Tensor, out_dtype: torch.dtype = torch.float32,
+                              stream=None) -> torch.Tensor:
+        """Every query head attends over its KV group's page list (tensor-core kernel)."""
+        q = self._check_q(q)
+        batch = q.shape[0]
+        out = torch.empty((batch, self.num_q_heads, self.head_dim), dtype=out_dtype,
+                          device=self.device)
+        dt = _lib.QK_DTYPE_F32 if out_dtype == torch.float32 else _lib.QK_DTYPE_F16
+        pages = pages.to(torch.int32).contiguous()
+        counts = counts.to(torch.int32).contiguous()
+        check(self._lib.qk_sparse_attend_grouped(self._h, layer, _ptr(q), batch, _ptr(pages),
+                                                 pages.shape[-1], _ptr(counts), _ptr(out), dt,
+                                                 _stream_ptr(stream)))
+        return out
+
+    def decode_step_grouped(self, layer: int, q: torch.Tensor, k: Optional[torch.Tensor],
+                            v: Optional[torch.Tensor], token_budget: int,
+                            group_reduce: str = "max", force_include_recent: bool = True,
+                            per_layer_enabled: bool = True, out: Optional[torch.Tensor] = None,
+                            pages: Optional[torch.Tensor] = None,
+                            counts: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+        """append -> estimate -> group top-K -> group attention (qk_decode_step_grouped)."""
+        q = self._check_q(q)
+        batch = q.shape[0]
+        if k is not None:
+            k = self._check_half(k, (batch, self.num_kv_heads, self.head_dim), "k")
+            v = self._check_half(v, (batch, self.num_kv_heads, self.head_dim), "v")
+        if out is None:
+            out = torch.empty((batch, self.num_q_heads, self.head_dim), dtype=torch.float32,
+                              device=self.device)
+        dt = _lib.QK_DTYPE_F32 if out.dtype == torch.float32 else _lib.QK_DTYPE_F16
+        cfg = _sel_cfg(token_budget, force_include_recent, per_layer_enabled)
+        check(self._lib.qk_decode_step_grouped(
+            self._h, layer, _ptr(q), _ptr(k), _ptr(v), batch, ctypes.byref(cfg),
+            self._group_reduce(group_reduce), _ptr(out), dt, _ptr(pages),
+            0 if pages is None else pages.shape[-1], _ptr(counts), _stream_ptr(stream)))
+        return out
+
     def decode_step_host(self, layer: int, q: np.ndarray, k: Optional[np.ndarray],
                          v: Optional[np.ndarray], token_budget: int,
                          force_include_recent: bool = True, per_layer_enabled: bool = True,
