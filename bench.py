@@ -77,6 +77,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-native-e2e", action="store_true")
+    ap.add_argument("--group-select", choices=["none", "max", "sum"], default="none",
+                    help="GQA group-shared selection (SURVEY §8f item 3, opt-in variant): one "
+                         "page set per KV head from the max/sum of its query heads' scores")
     return ap.parse_args()
 
 
@@ -134,6 +137,10 @@ class Workload:
             "kv_heads": HKV, "head_dim": HEAD_DIM, "page_size": PAGE,
             "layers_per_step": self.NL, "batch_per_gpu": B if args.shard == "requests" else None,
             "global_batch": self.global_batch, "parallelism": par,
+            "selection": ("per query head (the reference's semantics)"
+                          if args.group_select == "none" else
+                          f"GQA group-shared, group score = {args.group_select} over the query "
+                          "heads (opt-in variant, SURVEY §8f item 3)"),
             "l2": f"inputs larger than L2: {self.NL} rotating layer caches, each revisited after "
                   f"{self.NL - 1} other layers' traffic",
         }
@@ -397,15 +404,23 @@ def run_ours(args):
     for bb in range(lb):
         warm.prefill(0, bb, kn[0, 0, bb].view(lkv, 1, HEAD_DIM).contiguous(),
                      vn[0, 0, bb].view(lkv, 1, HEAD_DIM).contiguous())
-    warm.decode_step(0, qbuf[0], kbuf[0], vbuf[0], budget, stream=stream)
+    grouped = args.group_select != "none"
+
+    def decode(cache, layer, qq, kk, vv, o=None, pages=None, counts=None):
+        if grouped:
+            return cache.decode_step_grouped(layer, qq, kk, vv, budget, args.group_select, out=o,
+                                             pages=pages, counts=counts, stream=stream)
+        return cache.decode_step(layer, qq, kk, vv, budget, out=o, pages=pages, counts=counts,
+                                 stream=stream)
+
+    decode(warm, 0, qbuf[0], kbuf[0], vbuf[0])
     stream.synchronize()
     warm.close()
     launches0 = qc.kernel_launches
     graph = torch.cuda.CUDAGraph()
     with torch.cuda.graph(graph, stream=stream):
         for layer in range(NL):
-            qc.decode_step(layer, qbuf[layer], kbuf[layer], vbuf[layer], budget, out=out[layer],
-                           stream=stream)
+            decode(qc, layer, qbuf[layer], kbuf[layer], vbuf[layer], o=out[layer])
     kernels_per_step = qc.kernel_launches - launches0
 
     def step(i):
@@ -449,7 +464,7 @@ def run_ours(args):
     # GQA: the K/V term counts the union of the pages a KV head's query heads selected,
     # measured on the final state (one extra, untimed, non-appending step per layer).
     union = None
-    if G > 1:
+    if G > 1 and not grouped:  # grouped: one shared page set per KV head (the MHA formula)
         pages = torch.full((lb, lq, max(1, budget // PAGE)), -1, dtype=torch.int32, device=dev)
         counts = torch.zeros((lb, lq), dtype=torch.int32, device=dev)
         L_now = qc.token_count(0, 0)
@@ -480,7 +495,8 @@ def run_ours(args):
     traffic = profiled_traffic() if args.config == "cfg2" and world == 1 else None
 
     # Per-kernel breakdown (one layer, eager, CUDA events) on the current state.
-    breakdown = kernel_breakdown(qc, q[0], NL, budget, stream) if rank == 0 and lb == 1 else {}
+    breakdown = (kernel_breakdown(qc, q[0], NL, budget, stream)
+                 if rank == 0 and lb == 1 and not grouped else {})
 
     # End to end through the public API with host buffers: H2D of q/k/v and D2H of the
     # fp32 output inside the timed region.
@@ -491,7 +507,7 @@ def run_ours(args):
     kh.copy_(kn[0].cpu())
     vh.copy_(vn[0].cpu())
     e2e_steps = max(1, args.e2e_steps)
-    if shards is None:
+    if shards is None and not grouped:
         # qk_decode_step_host: the kernel reads/writes pinned, mapped staging directly.
         oh = torch.empty((NL, lb, lq, HEAD_DIM), dtype=torch.float32).pin_memory()
         qn, kn_, vn_, on = qh.numpy(), kh.numpy(), vh.numpy(), oh.numpy()
@@ -518,8 +534,9 @@ def run_ours(args):
                 dq.copy_(qh[layer], non_blocking=True)
                 dk.copy_(kh[layer], non_blocking=True)
                 dv.copy_(vh[layer], non_blocking=True)
-                qc.decode_step(layer, dq, dk, dv, budget, out=lout, stream=stream)
-                full = gather_outputs(lout, shards, B, HKV, G) if world > 1 else lout
+                decode(qc, layer, dq, dk, dv, o=lout)
+                full = (gather_outputs(lout, shards, B, HKV, G) if world > 1 and shards
+                        else lout)
                 oh[layer].copy_(full, non_blocking=True)
             stream.synchronize()
 
@@ -533,7 +550,9 @@ def run_ours(args):
                 e2e_layer(layer)
         e2e_s = time.perf_counter() - t0
         e2e_path = ("Python QuestCache.decode_step on this rank's units + NCCL all-gather of the "
-                    "per-head outputs (shard.gather_outputs) per layer")
+                    "per-head outputs (shard.gather_outputs) per layer" if shards is not None else
+                    "Python QuestCache.decode_step_grouped per layer: H2D of q/k/v from pinned "
+                    "host memory, the step, D2H of the fp32 output")
         d2h = HQ * B * HEAD_DIM * 4 * NL
     if world > 1:
         t = torch.tensor([e2e_s], device=dev)
@@ -544,7 +563,7 @@ def run_ours(args):
         e2e_us /= world
     # The native host API (C++ questkv_b200::DeviceCache::decode_step_host), compiled here
     # against the in-tree library; it replaces the Python number when it builds and runs.
-    if world == 1 and not args.no_native_e2e and args.config == "cfg2":
+    if world == 1 and not args.no_native_e2e and args.config == "cfg2" and not grouped:
         native = native_e2e(ctx, budget)
         if native is not None:
             e2e_us = native
@@ -596,7 +615,10 @@ def run_ours(args):
             "traffic": traffic,
             "frac_physical": (round(traffic / (us_per_layer * 1e-6) / 1e9 / peak, 4)
                               if traffic else None),
-            "kernel": "decode_fused_kernel (one launch = append+estimate+top-K+attend of a layer)",
+            "kernel": ("decode_fused_kernel (one launch = append+estimate+top-K+attend of a layer)"
+                       if not grouped else
+                       "append_kernel + estimate_kernel + group_topk_kernel + "
+                       "grouped_attend_kernel (mma.sync) per layer"),
             "timing": "per-layer time of the CUDA-graph replay (launch gaps included), CUDA "
                       "events on the launching stream, max over ranks",
             "bytes_per_launch": int(bytes_per_layer),
@@ -635,8 +657,9 @@ def native_e2e(ctx, budget):
 
 
 def kernel_breakdown(qc, q0, NL, budget, stream):
-    """Device time per layer of the separate (unfused) ops on the current caches: eager
-    launches, CUDA events, outputs preallocated, one untimed pass first."""
+    """Device time per layer of the separate (unfused) ops on the current caches: each op's
+    launches over n layers captured in a CUDA graph and replayed (so host dispatch is not
+    timed), CUDA events on the stream, outputs preallocated, one untimed replay first."""
     import torch
 
     n = min(8, NL)
@@ -661,20 +684,27 @@ def kernel_breakdown(qc, q0, NL, budget, stream):
     res = {}
     names = ("estimate", "select_topk", "sparse_attend", "dense_attend")
     with torch.cuda.stream(stream):
-        for name in names:  # warm: module load, allocator
+        for name in names:  # eager first: module load, real selections for the attend graphs
             for layer in range(n):
                 run(name, layer)
         stream.synchronize()
         for name in names:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                for layer in range(n):
+                    run(name, layer)
+            g.replay()
+            stream.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            for layer in range(n):
-                run(name, layer)
+            for _ in range(4):
+                g.replay()
             e1.record(stream)
             stream.synchronize()
-            res[name] = round(e0.elapsed_time(e1) * 1e3 / n, 2)
-    res["note"] = ("unfused ops, eager launches (launch gaps included), same caches; the "
-                   "bench step uses the fused kernel")
+            res[name] = round(e0.elapsed_time(e1) * 1e3 / (4 * n), 2)
+    res["note"] = ("unfused ops (the reference-style separate calls), each op over 8 layers "
+                   "captured in a CUDA graph (kernel + in-graph launch gap per layer), same caches; "
+                   "the bench step uses the fused kernel")
     return res
 
 

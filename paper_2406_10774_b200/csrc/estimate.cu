@@ -39,147 +39,274 @@ __device__ __forceinline__ double h2d_scaled(unsigned short h) {
     return __hiloint2double(int(t + s * 63u), 0);
 }
 
-constexpr int kThreads = 128;
-constexpr int kGroups = 4;
+// ---- MHA (G = 1): channel-split, certified -------------------------------------------------
+//
+// Thread (cg, pb) of a 256-thread CTA covers pages page0 + 8*pb .. +7 over the channel group
+// cg (D/8 channels): one 16-byte load of the sign-selected row per channel (8 pages), all of
+// them in flight at once, then 8 independent chains.  The 8 channel-group partials of a page
+// meet in shared memory and are added pairwise; every partial is a sum of exact products,
+// so the result is bitwise the reference's sequential sum whenever the page's magnitude
+// record certifies that no partial sum can round (sum|q| * max|x| < 2^(53 + uq + ux), as
+// the fused kernel, decode.cu); a failing page reruns the reference's chain.  Odd channels
+// convert with the exact integer construction scaled by 2^-1008 (weights pre-scaled by
+// 2^1008), even ones with F2F, so the XU and ALU pipes share the conversions.
+constexpr int kMhaThreads = 256;
+constexpr int kMhaPPC = 256;  // pages per CTA: 32 page blocks x 8 channel groups
 
-template <int D, int G, int PAGES>
+template <int D>
+__global__ void __launch_bounds__(kMhaThreads)
+estimate_mha_kernel(const __half* __restrict__ meta, const uint32_t* __restrict__ prange,
+                    const int32_t* __restrict__ len, const __half* __restrict__ q,
+                    double* __restrict__ scores, uint32_t layer, uint32_t B, uint32_t Hkv,
+                    uint32_t S, uint32_t head_dim, size_t slice_meta, uint32_t mrow,
+                    uint32_t sstride) {
+    constexpr int CPG = D / 8;                     // channels per group
+    constexpr int ROUND = CPG < 16 ? CPG : 16;     // loads in flight per round
+    __shared__ double dq[D], dw[D];
+    __shared__ unsigned char need[D];
+    __shared__ double part[8][kMhaPPC];
+    __shared__ double s_qpart[D / 32];
+    __shared__ unsigned int s_qcodep[D / 32];
+
+    const uint32_t bh = blockIdx.y;
+    const uint32_t b = bh / Hkv, kvh = bh % Hkv;
+    const uint32_t n_tok = static_cast<uint32_t>(len[layer * B + b]);
+    const uint32_t P = (n_tok + S - 1) / S;
+    const uint32_t page0 = blockIdx.x * kMhaPPC;
+    if (page0 >= P) return;
+    const int tid = threadIdx.x, lane = tid & 31;
+    if (tid < D) {
+        const __half h = tid < int(head_dim) ? q[(size_t(b) * Hkv + kvh) * head_dim + tid]
+                                             : __float2half(0.0f);
+        const double x = double(__half2float(h));
+        dq[tid] = x;
+        dw[tid] = (tid & 1) ? x * 0x1p1008 : x;
+        need[tid] = (x < 0.0) ? 0 : 1;  // the row index: min (0) or max (1)
+        double a = fabs(x);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        const unsigned int code = __reduce_min_sync(0xffffffffu, ulp_code(__half_as_ushort(h)));
+        if (lane == 0) {
+            s_qpart[tid >> 5] = a;
+            s_qcodep[tid >> 5] = code;
+        }
+    }
+    __syncthreads();
+
+    const size_t s = (size_t(layer) * B + b) * Hkv + kvh;
+    const __half* mslice = meta + s * slice_meta;  // [2][D][mrow]
+    const int cg = tid >> 5, pb = lane;            // warp = channel group: 512-byte loads
+    const uint32_t pbase = page0 + uint32_t(pb) * 8;
+    const bool act = pbase < P;
+    double acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+#pragma unroll
+    for (int r0 = 0; r0 < CPG; r0 += ROUND) {
+        int4 v[ROUND];
+#pragma unroll
+        for (int k = 0; k < ROUND; ++k) {
+            const int c = cg * CPG + r0 + k;
+            v[k] = act ? ld_nc_v4(mslice + (size_t(need[c]) * D + c) * mrow + pbase)
+                       : make_int4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int k = 0; k < ROUND; ++k) {
+            const int c = cg * CPG + r0 + k;
+            const double w = dw[c];
+            const unsigned short* h = reinterpret_cast<const unsigned short*>(&v[k]);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                acc[j] = __fma_rn(w, (c & 1) ? h2d_scaled(h[j]) : h2d(__ushort_as_half(h[j])), acc[j]);
+        }
+    }
+    double2* dst = reinterpret_cast<double2*>(&part[cg][pb * 8]);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) dst[j] = make_double2(acc[2 * j], acc[2 * j + 1]);
+    __syncthreads();
+
+    const uint32_t p = page0 + uint32_t(tid);
+    if (p >= P || p >= sstride) return;
+    double sc = ((part[0][tid] + part[1][tid]) + (part[2][tid] + part[3][tid])) +
+                ((part[4][tid] + part[5][tid]) + (part[6][tid] + part[7][tid]));
+    double qabs = 0.0;
+    unsigned int qcode = 31u;
+#pragma unroll
+    for (int w = 0; w < D / 32; ++w) {
+        qabs += s_qpart[w];
+        qcode = min(qcode, s_qcodep[w]);
+    }
+    const uint32_t rec = __ldg(prange + s * mrow + p);
+    const uint32_t xcode = rec >> 16;
+    bool exact = xcode >= 31u || qcode >= 31u;  // all-zero operands
+    if (!exact) {
+        const double bound =
+            __dmul_ru(qabs, double(__half2float(__ushort_as_half(uint16_t(rec & 0x7fffu)))));
+        const int e = 5 + int(qcode) + int(xcode);
+        exact = bound < __longlong_as_double(static_cast<long long>(e + 1023) << 52);
+    }
+    if (!exact) {  // the reference's sequential chain (criticality.cpp:16-21)
+        double a = 0.0;
+        for (int c = 0; c < D; ++c)
+            a = __fma_rn(dq[c], h2d(mslice[(size_t(need[c]) * D + c) * mrow + p]), a);
+        sc = a;
+    }
+    scores[(size_t(b) * Hkv + kvh) * sstride + p] = sc;
+}
+
+// ---- GQA (G > 1): sequential chains, the reference's order exactly ------------------------
+//
+// Thread = PB consecutive pages x all G query heads of one (sequence, KV head): per channel
+// one 16-byte (8-page) load of each row some head needs, every value converted once (min
+// row with F2F, max row with the scaled integer construction) and folded into the
+// PB * G independent chains (enough to cover the DFMA latency; no certificate needed).
+// The next channel group's loads are in flight while the current one is folded.
+constexpr int kThreads = 128;
+
+template <int G>
+struct GqaGeom {
+    static constexpr int PB = (G >= 8) ? 4 : 8;   // pages per thread (one 8/16-byte load)
+    static constexpr int PPC = kThreads * PB;      // pages per CTA
+    static constexpr int UNROLL = 4;               // channels per pipeline stage
+};
+
+template <int PB>
+struct Piece;
+template <>
+struct Piece<8> {
+    int4 v;
+    __device__ __forceinline__ void load(const __half* p) { v = ld_nc_v4(p); }
+    __device__ __forceinline__ void zero() { v = make_int4(0, 0, 0, 0); }
+    __device__ __forceinline__ unsigned short at(int j) const {
+        return reinterpret_cast<const unsigned short*>(&v)[j];
+    }
+};
+template <>
+struct Piece<4> {
+    int2 v;
+    __device__ __forceinline__ void load(const __half* p) {
+        asm volatile("ld.global.nc.L1::no_allocate.v2.s32 {%0,%1}, [%2];"
+                     : "=r"(v.x), "=r"(v.y) : "l"(p));
+    }
+    __device__ __forceinline__ void zero() { v = make_int2(0, 0); }
+    __device__ __forceinline__ unsigned short at(int j) const {
+        return reinterpret_cast<const unsigned short*>(&v)[j];
+    }
+};
+
+template <int D, int G>
 __global__ void __launch_bounds__(kThreads)
-estimate_kernel(const __half* __restrict__ meta, const int32_t* __restrict__ len,
-                const __half* __restrict__ q, double* __restrict__ scores, uint32_t layer,
-                uint32_t B, uint32_t Hkv, uint32_t S, uint32_t head_dim, size_t slice_meta,
-                uint32_t mrow, uint32_t sstride) {
-    constexpr int NROW = (G == 1) ? 1 : 2;  // metadata rows staged per channel
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    __half* rows = reinterpret_cast<__half*>(smem_raw);                 // [NROW][D][PAGES]
-    double* dq = reinterpret_cast<double*>(rows + NROW * D * PAGES);    // [G][D]
+estimate_gqa_kernel(const __half* __restrict__ meta, const int32_t* __restrict__ len,
+                    const __half* __restrict__ q, double* __restrict__ scores, uint32_t layer,
+                    uint32_t B, uint32_t Hkv, uint32_t S, uint32_t head_dim, size_t slice_meta,
+                    uint32_t mrow, uint32_t sstride) {
+    using GM = GqaGeom<G>;
+    constexpr int PB = GM::PB, PPC = GM::PPC, U = GM::UNROLL;
+    __shared__ double dw[G * D];  // weights of the conversion path (max row scaled 2^1008)
     __shared__ unsigned char need[D];  // bit0: max row needed, bit1: min row needed
 
     const uint32_t bh = blockIdx.y;
     const uint32_t b = bh / Hkv, kvh = bh % Hkv;
     const uint32_t n_tok = static_cast<uint32_t>(len[layer * B + b]);
     const uint32_t P = (n_tok + S - 1) / S;
-    const uint32_t page0 = blockIdx.x * PAGES;
+    const uint32_t page0 = blockIdx.x * PPC;
     if (page0 >= P) return;
-    const uint32_t npg = min(uint32_t(PAGES), P - page0);
-    const int n8 = int((npg + 7) / 8);  // 16-byte pieces per channel row
-
-    // Query of the G heads sharing this KV head, widened to double (exact).
-    for (int i = threadIdx.x; i < G * D; i += kThreads) {
+    const int tid = threadIdx.x;
+    for (int i = tid; i < G * D; i += kThreads) {
         const int g = i / D, c = i % D;
-        const size_t qh = size_t(kvh) * G + g;
-        const float x = c < int(head_dim)
-                            ? __half2float(q[(size_t(b) * Hkv * G + qh) * head_dim + c])
-                            : 0.0f;
-        dq[g * D + c] = double(x);
-        if (G == 1) dq[D + c] = double(x) * 0x1p1008;  // weight of the scaled path
+        const double x = c < int(head_dim)
+                             ? double(__half2float(q[(size_t(b) * Hkv * G + size_t(kvh) * G + g) * head_dim + c]))
+                             : 0.0;
+        dw[i] = (x < 0.0) ? x : x * 0x1p1008;
     }
     __syncthreads();
-    for (int c = threadIdx.x; c < D; c += kThreads) {
+    for (int c = tid; c < D; c += kThreads) {
         unsigned char m = 0;
 #pragma unroll
-        for (int g = 0; g < G; ++g) m |= (dq[g * D + c] < 0.0) ? 2 : 1;
+        for (int g = 0; g < G; ++g) m |= (dw[g * D + c] < 0.0) ? 2 : 1;
         need[c] = m;
     }
     __syncthreads();
 
+    const uint32_t pbase = page0 + uint32_t(tid) * PB;
+    if (pbase >= P) return;
     const size_t s = (size_t(layer) * B + b) * Hkv + kvh;
-    const __half* mslice = meta + s * slice_meta;
-    constexpr int CH_PER_GROUP = D / kGroups;
+    const __half* mslice = meta + s * slice_meta;  // [2][D][mrow]
+    double acc[G][PB];
 #pragma unroll
-    for (int grp = 0; grp < kGroups; ++grp) {
-        const int n_items = CH_PER_GROUP * NROW * n8;
-        for (int i = threadIdx.x; i < n_items; i += kThreads) {
-            const int piece = i % n8;
-            const int rest = i / n8;
-            const int r = rest % NROW;
-            const int c = grp * CH_PER_GROUP + rest / NROW;
-            // G == 1: the single staged row is the one the query's sign selects.
-            const int minmax = (G == 1) ? ((need[c] & 2) ? 0 : 1) : r;
-            if (G > 1 && !(need[c] & (minmax == 0 ? 2 : 1))) continue;
-            const __half* src = mslice + (size_t(minmax) * D + c) * mrow + page0 + piece * 8;
-            __half* dst = rows + (size_t(r) * D + c) * PAGES + piece * 8;
-            cp_async16(dst, src);
-        }
-        cp_async_commit();
-    }
+    for (int g = 0; g < G; ++g)
+#pragma unroll
+        for (int j = 0; j < PB; ++j) acc[g][j] = 0.0;
 
-    if constexpr (G == 1) {
-        const int j = threadIdx.x * 2;  // two adjacent pages
-        const bool active = uint32_t(j) < npg;
-        double acc0 = 0.0, acc1 = 0.0;
+    Piece<PB> lo[2][U], hi[2][U];
+    auto load = [&](int buf, int c0) {
 #pragma unroll
-        for (int grp = 0; grp < kGroups; ++grp) {
-            if (grp == 0) cp_async_wait<kGroups - 1>();
-            if (grp == 1) cp_async_wait<kGroups - 2>();
-            if (grp == 2) cp_async_wait<kGroups - 3>();
-            if (grp == 3) cp_async_wait<0>();
-            __syncthreads();
-            if (active) {
-#pragma unroll 8
-                for (int cc = 0; cc < CH_PER_GROUP; ++cc) {
-                    const int c = grp * CH_PER_GROUP + cc;
-                    const __half2 h2 = *reinterpret_cast<const __half2*>(rows + size_t(c) * PAGES + j);
-                    // Page 2j converts on the XU pipe, page 2j+1 with integer ops
-                    // (h2d_scaled, weight pre-scaled by 2^1008): both pipes share the work.
-                    acc0 = __fma_rn(dq[c], h2d(__low2half(h2)), acc0);
-                    acc1 = __fma_rn(dq[D + c], h2d_scaled(__half_as_ushort(__high2half(h2))), acc1);
+        for (int u = 0; u < U; ++u) {
+            const int c = c0 + u;
+            const unsigned char m = need[c];
+            if (m & 2) lo[buf][u].load(mslice + size_t(c) * mrow + pbase);
+            else lo[buf][u].zero();
+            if (m & 1) hi[buf][u].load(mslice + size_t(D + c) * mrow + pbase);
+            else hi[buf][u].zero();
+        }
+    };
+    auto fold = [&](int buf, int c0) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int c = c0 + u;
+            double xl[PB], xh[PB];
+#pragma unroll
+            for (int j = 0; j < PB; ++j) {
+                xl[j] = h2d(__ushort_as_half(lo[buf][u].at(j)));
+                xh[j] = h2d_scaled(hi[buf][u].at(j));
+            }
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const double w = dw[g * D + c];
+                if (w < 0.0) {  // uniform over the CTA: a branch, not selects
+#pragma unroll
+                    for (int j = 0; j < PB; ++j) acc[g][j] = __fma_rn(w, xl[j], acc[g][j]);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < PB; ++j) acc[g][j] = __fma_rn(w, xh[j], acc[g][j]);
                 }
             }
         }
-        const uint32_t p = page0 + j;
-        double* out = scores + (size_t(b) * Hkv + kvh) * sstride;
-        if (active && p < P && p < sstride) out[p] = acc0;
-        if (active && p + 1 < P && p + 1 < sstride) out[p + 1] = acc1;
-    } else {
-        const int j = threadIdx.x;  // PAGES == kThreads pages per CTA
-        const bool active = uint32_t(j) < npg;
-        double acc[G];
+    };
+    load(0, 0);
+#pragma unroll 1
+    for (int c0 = 0; c0 < D; c0 += 2 * U) {
+        if (c0 + U < D) load(1, c0 + U);
+        fold(0, c0);
+        if (c0 + U >= D) break;
+        if (c0 + 2 * U < D) load(0, c0 + 2 * U);
+        fold(1, c0 + U);
+    }
 #pragma unroll
-        for (int g = 0; g < G; ++g) acc[g] = 0.0;
+    for (int j = 0; j < PB; ++j) {
+        const uint32_t p = pbase + j;
+        if (p >= P || p >= sstride) break;
 #pragma unroll
-        for (int grp = 0; grp < kGroups; ++grp) {
-            if (grp == 0) cp_async_wait<kGroups - 1>();
-            if (grp == 1) cp_async_wait<kGroups - 2>();
-            if (grp == 2) cp_async_wait<kGroups - 3>();
-            if (grp == 3) cp_async_wait<0>();
-            __syncthreads();
-            if (active) {
-#pragma unroll 4
-                for (int cc = 0; cc < CH_PER_GROUP; ++cc) {
-                    const int c = grp * CH_PER_GROUP + cc;
-                    const double lo = h2d(rows[(size_t(0) * D + c) * PAGES + j]);
-                    const double hi = h2d(rows[(size_t(1) * D + c) * PAGES + j]);
-#pragma unroll
-                    for (int g = 0; g < G; ++g) {
-                        const double w = dq[g * D + c];
-                        acc[g] = __fma_rn(w, (w < 0.0) ? lo : hi, acc[g]);
-                    }
-                }
-            }
-        }
-        const uint32_t p = page0 + j;
-        if (active && p < P && p < sstride) {
-#pragma unroll
-            for (int g = 0; g < G; ++g)
-                scores[(size_t(b) * Hkv * G + size_t(kvh) * G + g) * sstride + p] = acc[g];
-        }
+        for (int g = 0; g < G; ++g)
+            scores[(size_t(b) * Hkv * G + size_t(kvh) * G + g) * sstride + p] = acc[g][j];
     }
 }
 
-template <int D, int G, int PAGES>
+template <int D, int G>
 int run(const qk_cache* c, uint32_t layer, const __half* q, uint32_t batch, double* scores,
         uint32_t stride, uint32_t max_pages, cudaStream_t st) {
-    constexpr int NROW = (G == 1) ? 1 : 2;
-    const size_t smem = size_t(NROW) * D * PAGES * sizeof(__half) +
-                        size_t(G == 1 ? 2 : G) * D * sizeof(double);
-    auto kern = estimate_kernel<D, G, PAGES>;
-    if (int rc = ensure_func_attrs(reinterpret_cast<const void*>(kern), smem, c->desc.device, false,
-                                   "estimate_kernel attributes"))
-        return rc;
-    const uint32_t pages_per_cta = PAGES;
-    const dim3 grid((max_pages + pages_per_cta - 1) / pages_per_cta, batch * c->Hkv);
-    kern<<<grid, kThreads, smem, st>>>(c->meta, c->d_len, q, scores, layer, c->B, c->Hkv, c->S,
-                                       c->desc.head_dim, c->slice_meta, c->Mrow, stride);
+    if constexpr (G == 1) {
+        const dim3 grid((max_pages + kMhaPPC - 1) / kMhaPPC, batch * c->Hkv);
+        estimate_mha_kernel<D><<<grid, kMhaThreads, 0, st>>>(
+            c->meta, c->prange, c->d_len, q, scores, layer, c->B, c->Hkv, c->S, c->desc.head_dim,
+            c->slice_meta, c->Mrow, stride);
+    } else {
+        using GM = GqaGeom<G>;
+        const dim3 grid((max_pages + GM::PPC - 1) / GM::PPC, batch * c->Hkv);
+        estimate_gqa_kernel<D, G><<<grid, kThreads, 0, st>>>(
+            c->meta, c->d_len, q, scores, layer, c->B, c->Hkv, c->S, c->desc.head_dim,
+            c->slice_meta, c->Mrow, stride);
+    }
     const_cast<qk_cache*>(c)->launches++;
     return cuda_check(cudaGetLastError(), "estimate_kernel");
 }
@@ -188,10 +315,10 @@ template <int D>
 int dispatch_g(const qk_cache* c, uint32_t layer, const __half* q, uint32_t batch,
                double* scores, uint32_t stride, uint32_t max_pages, cudaStream_t st) {
     switch (c->G) {
-        case 1: return run<D, 1, 2 * kThreads>(c, layer, q, batch, scores, stride, max_pages, st);
-        case 2: return run<D, 2, kThreads>(c, layer, q, batch, scores, stride, max_pages, st);
-        case 4: return run<D, 4, kThreads>(c, layer, q, batch, scores, stride, max_pages, st);
-        case 8: return run<D, 8, kThreads>(c, layer, q, batch, scores, stride, max_pages, st);
+        case 1: return run<D, 1>(c, layer, q, batch, scores, stride, max_pages, st);
+        case 2: return run<D, 2>(c, layer, q, batch, scores, stride, max_pages, st);
+        case 4: return run<D, 4>(c, layer, q, batch, scores, stride, max_pages, st);
+        case 8: return run<D, 8>(c, layer, q, batch, scores, stride, max_pages, st);
         default: return set_error(QK_ERR_UNSUPPORTED, "qk_estimate: GQA group size must be 1, 2, 4 or 8");
     }
 }

@@ -31,7 +31,7 @@
 //     by the last CTA (attend.cu's split rule, ticket and merge).
 #include <math_constants.h>
 
-#include "select.cuh"
+#include "topk_rows.cuh"
 
 namespace qk {
 namespace {
@@ -88,6 +88,7 @@ group_topk_kernel(const double* __restrict__ scores, uint32_t sstride,
 
 constexpr int kThreads = 128;
 constexpr int kWarps = kThreads / 32;
+constexpr int kListCap = 256;  // page-list entries of a split staged in shared memory
 
 __device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a2, uint32_t b0,
                                          uint32_t b1) {
@@ -109,7 +110,7 @@ __device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
 }
 
 template <int D, int G>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 2)
 grouped_attend_kernel(const __half* __restrict__ kp, const __half* __restrict__ vp,
                       const int32_t* __restrict__ len, const __half* __restrict__ q,
                       const int32_t* __restrict__ pages, uint32_t pstride,
@@ -117,7 +118,7 @@ grouped_attend_kernel(const __half* __restrict__ kp, const __half* __restrict__ 
                       uint32_t Hkv, uint32_t S, uint32_t head_dim, size_t slice_kv,
                       float scale_log2, float* __restrict__ ws_partial,
                       int32_t* __restrict__ ws_ticket, void* __restrict__ out, int out_dtype,
-                      int32_t* __restrict__ status) {
+                      int32_t* __restrict__ status, int min_pps) {
     static_assert(G >= 1 && G <= 8, "at most 8 query heads per group (MMA rows 0..7)");
     constexpr int KS = D / 16;   // k-steps of S = Q K^T
     constexpr int NT = D / 8;    // n-tiles (8 channels) of O = P V
@@ -137,7 +138,7 @@ grouped_attend_kernel(const __half* __restrict__ kp, const __half* __restrict__ 
         if (blockIdx.x == 0 && threadIdx.x == 0) record_status(status, QK_DEV_EMPTY_SELECTION);
         return;
     }
-    const int pps = max(kMinPagesPerSplit, (count + kMaxSplits - 1) / kMaxSplits);
+    const int pps = max(min_pps, (count + kMaxSplits - 1) / kMaxSplits);
     const int nsplit = (count + pps - 1) / pps;
     if (uint32_t(count) > pstride || nsplit > int(gridDim.x)) {
         if (blockIdx.x == 0 && threadIdx.x == 0) record_status(status, QK_DEV_BAD_COUNT);
@@ -184,86 +185,135 @@ grouped_attend_kernel(const __half* __restrict__ kp, const __half* __restrict__ 
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) o[nt][0] = o[nt][1] = 0.0f;
 
-    for (int i = first + warp; i < last; i += kWarps) {
+    // Chunks (16 tokens of a page) of this warp's pages [first + warp, last; kWarps), walked
+    // with the next chunk's K/V loads in flight while the current one is folded.
+    struct Chunk {
+        int4 ka[KCH], kb[KCH], va[4][VCH];
+        uint32_t n;  // valid rows of the chunk (0: nothing to fold)
+    };
+    // The CTA's page list, validated once (sparse_attention's checks, attention.cpp:99-106):
+    // invalid entries are recorded and skipped.
+    __shared__ int32_t s_pg[kListCap];
+    const bool in_smem = last - first <= kListCap;
+    for (int i = first + tid; i < last && in_smem; i += kThreads) {
         const int pg = plist[i];
-        if (pg < 0 || uint32_t(pg) >= P || (i > 0 && plist[i - 1] >= pg)) {
-            if (lane == 0)
-                record_status(status, (pg < 0 || uint32_t(pg) >= P) ? QK_DEV_PAGE_OUT_OF_RANGE
-                                                                    : QK_DEV_PAGE_NOT_ASCENDING);
-            continue;
-        }
-        const uint32_t plen = min(S, n_tok - uint32_t(pg) * S);
-        const __half* kpage = kslice + size_t(pg) * S * D;
-        const __half* vpage = vslice + size_t(pg) * S * D;
-        for (uint32_t t0 = 0; t0 < plen; t0 += 16) {
+        const bool bad_range = pg < 0 || uint32_t(pg) >= P;
+        const bool bad_order = i > 0 && plist[i - 1] >= pg;
+        if (bad_range || bad_order)
+            record_status(status, bad_range ? QK_DEV_PAGE_OUT_OF_RANGE : QK_DEV_PAGE_NOT_ASCENDING);
+        s_pg[i - first] = (bad_range || bad_order) ? -1 : pg;
+    }
+    __syncthreads();
+    int ci = first + warp;  // page list position of the chunk to load next
+    uint32_t ct0 = 0;       // its first row within the page
+    auto load = [&](Chunk& ch) {
+        ch.n = 0;
+        while (ci < last) {
+            int pg;
+            if (in_smem) {
+                pg = s_pg[ci - first];
+            } else {
+                pg = plist[ci];
+                if (pg < 0 || uint32_t(pg) >= P || (ci > 0 && plist[ci - 1] >= pg)) {
+                    if (lane == 0)
+                        record_status(status, (pg < 0 || uint32_t(pg) >= P) ? QK_DEV_PAGE_OUT_OF_RANGE
+                                                                            : QK_DEV_PAGE_NOT_ASCENDING);
+                    pg = -1;
+                }
+            }
+            if (pg < 0) {
+                ci += kWarps;
+                ct0 = 0;
+                continue;
+            }
+            const uint32_t plen = min(S, n_tok - uint32_t(pg) * S);
+            const uint32_t t0 = ct0;
+            const uint32_t n = min(16u, plen - t0);
+            const __half* kpage = kslice + (size_t(pg) * S + t0) * D;
+            const __half* vpage = vslice + (size_t(pg) * S + t0) * D;
             // K rows r and r+8 (chunks 4j + c); V rows 2c, 2c+1, 2c+8, 2c+9 (channels NT*r..).
-            int4 ka[KCH], kb[KCH], va[4][VCH];
-            const uint32_t ra = t0 + r, rb = t0 + r + 8;
 #pragma unroll
             for (int j = 0; j < KCH; ++j) {
-                ka[j] = ra < plen ? ld_nc_v4(kpage + size_t(ra) * D + 8 * (4 * j + c)) : make_int4(0, 0, 0, 0);
-                kb[j] = rb < plen ? ld_nc_v4(kpage + size_t(rb) * D + 8 * (4 * j + c)) : make_int4(0, 0, 0, 0);
+                ch.ka[j] = uint32_t(r) < n ? ld_nc_v4(kpage + size_t(r) * D + 8 * (4 * j + c))
+                                           : make_int4(0, 0, 0, 0);
+                ch.kb[j] = uint32_t(r + 8) < n ? ld_nc_v4(kpage + size_t(r + 8) * D + 8 * (4 * j + c))
+                                               : make_int4(0, 0, 0, 0);
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const uint32_t row = t0 + 2 * c + (u & 1) + 8 * (u >> 1);
+                const uint32_t row = 2 * c + (u & 1) + 8 * (u >> 1);
 #pragma unroll
                 for (int x = 0; x < VCH; ++x)
-                    va[u][x] = row < plen ? ld_nc_v4(vpage + size_t(row) * D + NT * r + 8 * x)
+                    ch.va[u][x] = row < n ? ld_nc_v4(vpage + size_t(row) * D + NT * r + 8 * x)
                                           : make_int4(0, 0, 0, 0);
             }
-            // S = Q K^T: n-tile 0 = tokens 0..7, n-tile 1 = tokens 8..15 of the chunk.
-            float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-            for (int j = 0; j < KCH; ++j) {
-#pragma unroll
-                for (int t = 0; t < 2; ++t) {
-                    mma16816(s0, qa[2 * j + t][0], qa[2 * j + t][1], word(ka[j], 2 * t), word(ka[j], 2 * t + 1));
-                    mma16816(s1, qa[2 * j + t][0], qa[2 * j + t][1], word(kb[j], 2 * t), word(kb[j], 2 * t + 1));
-                }
+            ch.n = n;
+            if (t0 + 16 < plen) {
+                ct0 = t0 + 16;
+            } else {
+                ci += kWarps;
+                ct0 = 0;
             }
-            // Head r's logits of tokens 2c, 2c+1, 8+2c, 9+2c (base 2, masked past plen).
-            float x[4];
-            x[0] = (t0 + 2 * c < plen) ? s0[0] * scale_log2 : -CUDART_INF_F;
-            x[1] = (t0 + 2 * c + 1 < plen) ? s0[1] * scale_log2 : -CUDART_INF_F;
-            x[2] = (t0 + 2 * c + 8 < plen) ? s1[0] * scale_log2 : -CUDART_INF_F;
-            x[3] = (t0 + 2 * c + 9 < plen) ? s1[1] * scale_log2 : -CUDART_INF_F;
-            float mx = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3]));
-            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-            const float m_new = fmaxf(m, mx);
-            const float alpha = exp2f(m - m_new);  // 0 on the first chunk
-            float p[4];
+            return;
+        }
+    };
+    auto fold = [&](const Chunk& ch) {
+        const uint32_t n = ch.n;
+        // S = Q K^T: n-tile 0 = tokens 0..7, n-tile 1 = tokens 8..15 of the chunk.
+        float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-            for (int e = 0; e < 4; ++e) p[e] = exp2f(x[e] - m_new);
-            l = l * alpha + ((p[0] + p[1]) + (p[2] + p[3]));
-            m = m_new;
+        for (int j = 0; j < KCH; ++j) {
 #pragma unroll
-            for (int nt = 0; nt < NT; ++nt) {
-                o[nt][0] *= alpha;
-                o[nt][1] *= alpha;
-            }
-            // P as A fragments (k = token 2c.. / 2c+8..), split into fp16 hi + lo.
-            const uint32_t ph0 = pack_h2(p[0], p[1]), ph2 = pack_h2(p[2], p[3]);
-            const __half2 h0 = *reinterpret_cast<const __half2*>(&ph0);
-            const __half2 h2 = *reinterpret_cast<const __half2*>(&ph2);
-            const uint32_t pl0 = pack_h2(p[0] - __low2float(h0), p[1] - __high2float(h0));
-            const uint32_t pl2 = pack_h2(p[2] - __low2float(h2), p[3] - __high2float(h2));
-            // O += P V: n-tile nt = channels NT*n + nt; B fragment = V[2c][ch], V[2c+1][ch] and
-            // V[2c+8][ch], V[2c+9][ch] of this lane's channel ch = NT*r + nt.
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt) {
-                const int x8 = nt / 8, w = (nt % 8) / 2;
-                const uint32_t sel = (nt & 1) ? 0x7632u : 0x5410u;
-                const uint32_t b0 = __byte_perm(word(va[0][x8], w), word(va[1][x8], w), sel);
-                const uint32_t b1 = __byte_perm(word(va[2][x8], w), word(va[3][x8], w), sel);
-                float acc[4] = {o[nt][0], o[nt][1], 0.f, 0.f};
-                mma16816(acc, ph0, ph2, b0, b1);
-                mma16816(acc, pl0, pl2, b0, b1);
-                o[nt][0] = acc[0];
-                o[nt][1] = acc[1];
+            for (int t = 0; t < 2; ++t) {
+                mma16816(s0, qa[2 * j + t][0], qa[2 * j + t][1], word(ch.ka[j], 2 * t), word(ch.ka[j], 2 * t + 1));
+                mma16816(s1, qa[2 * j + t][0], qa[2 * j + t][1], word(ch.kb[j], 2 * t), word(ch.kb[j], 2 * t + 1));
             }
         }
+        // Head r's logits of tokens 2c, 2c+1, 8+2c, 9+2c (base 2, masked past n).
+        float x[4];
+        x[0] = (uint32_t(2 * c) < n) ? s0[0] * scale_log2 : -CUDART_INF_F;
+        x[1] = (uint32_t(2 * c + 1) < n) ? s0[1] * scale_log2 : -CUDART_INF_F;
+        x[2] = (uint32_t(2 * c + 8) < n) ? s1[0] * scale_log2 : -CUDART_INF_F;
+        x[3] = (uint32_t(2 * c + 9) < n) ? s1[1] * scale_log2 : -CUDART_INF_F;
+        float mx = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3]));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        const float m_new = fmaxf(m, mx);  // finite: row 0 of a chunk is always valid
+        const float alpha = exp2f(m - m_new);  // 0 on the first chunk
+        float p[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) p[e] = exp2f(x[e] - m_new);
+        l = l * alpha + ((p[0] + p[1]) + (p[2] + p[3]));
+        m = m_new;
+        // P as A fragments (k = token 2c.. / 2c+8..), split into fp16 hi + lo.
+        const uint32_t ph0 = pack_h2(p[0], p[1]), ph2 = pack_h2(p[2], p[3]);
+        const __half2 h0 = *reinterpret_cast<const __half2*>(&ph0);
+        const __half2 h2 = *reinterpret_cast<const __half2*>(&ph2);
+        const uint32_t pl0 = pack_h2(p[0] - __low2float(h0), p[1] - __high2float(h0));
+        const uint32_t pl2 = pack_h2(p[2] - __low2float(h2), p[3] - __high2float(h2));
+        // O += P V: n-tile nt = channels NT*n + nt; B fragment = V[2c][ch], V[2c+1][ch] and
+        // V[2c+8][ch], V[2c+9][ch] of this lane's channel ch = NT*r + nt.
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+            const int x8 = nt / 8, w = (nt % 8) / 2;
+            const uint32_t sel = (nt & 1) ? 0x7632u : 0x5410u;
+            const uint32_t b0 = __byte_perm(word(ch.va[0][x8], w), word(ch.va[1][x8], w), sel);
+            const uint32_t b1 = __byte_perm(word(ch.va[2][x8], w), word(ch.va[3][x8], w), sel);
+            float acc[4] = {o[nt][0] * alpha, o[nt][1] * alpha, 0.f, 0.f};
+            mma16816(acc, ph0, ph2, b0, b1);
+            mma16816(acc, pl0, pl2, b0, b1);
+            o[nt][0] = acc[0];
+            o[nt][1] = acc[1];
+        }
+    };
+    Chunk c0, c1;  // two buffers, alternating roles (no register copies)
+    load(c0);
+    while (c0.n) {
+        load(c1);  // in flight during the fold
+        fold(c0);
+        if (!c1.n) break;
+        load(c0);
+        fold(c1);
     }
     // This warp's mass of head r: the four lanes of the row.
     l += __shfl_xor_sync(0xffffffffu, l, 1);
@@ -282,31 +332,42 @@ grouped_attend_kernel(const __half* __restrict__ kp, const __half* __restrict__ 
     __syncthreads();
 
     // CTA combine per head in warp order, then (multi-split) partials + last-CTA merge.
-    float* part_base = ws_partial + size_t(bk) * kMaxSplits * G * (D + 2);
-    for (int i = tid; i < G * D; i += kThreads) {
-        const int g = i / D, d = i % D;
+    __shared__ float s_w[kWarps][G], s_M[G], s_L[G];
+    __shared__ float s_sw[kMaxSplits][G];  // merge weights exp2(m_s - M) / L per split
+    if (tid < G) {
+        const int g = tid;
         float M = -CUDART_INF_F;
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) M = fmaxf(M, s_m[w][g]);
-        float L = 0.0f, acc = 0.0f;
+        float L = 0.0f;
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) {
             const float sc = (s_m[w][g] == -CUDART_INF_F) ? 0.0f : exp2f(s_m[w][g] - M);
+            s_w[w][g] = sc;
             L += s_l[w][g] * sc;
-            acc += s_o[w][g][d] * sc;
         }
+        s_M[g] = M;
+        s_L[g] = L;
+    }
+    __syncthreads();
+    float* part_base = ws_partial + size_t(bk) * kMaxSplits * G * (D + 2);
+    for (int i = tid; i < G * D; i += kThreads) {
+        const int g = i / D, d = i % D;
+        float acc = 0.0f;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) acc += s_o[w][g][d] * s_w[w][g];
         if (nsplit == 1) {
             if (d < int(head_dim)) {
                 const size_t oi = (size_t(b) * Hq + size_t(kvh) * G + g) * head_dim + d;
-                if (out_dtype == QK_DTYPE_F32) static_cast<float*>(out)[oi] = acc / L;
-                else static_cast<__half*>(out)[oi] = __float2half_rn(acc / L);
+                if (out_dtype == QK_DTYPE_F32) static_cast<float*>(out)[oi] = acc / s_L[g];
+                else static_cast<__half*>(out)[oi] = __float2half_rn(acc / s_L[g]);
             }
         } else {
             float* part = part_base + (size_t(split) * G + g) * (D + 2);
             part[2 + d] = acc;
             if (d == 0) {
-                part[0] = M;
-                part[1] = L;
+                part[0] = s_M[g];
+                part[1] = s_L[g];
             }
         }
     }
@@ -317,23 +378,35 @@ grouped_attend_kernel(const __half* __restrict__ kp, const __half* __restrict__ 
     __syncthreads();
     if (!s_last) return;
     __threadfence();
+    // Last CTA: every split's (m, l) in parallel, then per-head weights in split order.
+    for (int i = tid; i < nsplit * G; i += kThreads) {
+        const float* pp = part_base + size_t(i) * (D + 2);  // i = split * G + g
+        s_sw[i / G][i % G] = __ldcg(pp);
+    }
+    __syncthreads();
+    if (tid < G) {
+        const int g = tid;
+        float Mg = -CUDART_INF_F;
+        for (int sp = 0; sp < nsplit; ++sp) Mg = fmaxf(Mg, s_sw[sp][g]);
+        float Lg = 0.0f;
+        for (int sp = 0; sp < nsplit; ++sp) {
+            const float ms = s_sw[sp][g];
+            const float w = (ms == -CUDART_INF_F) ? 0.0f : exp2f(ms - Mg);
+            Lg += __ldcg(part_base + (size_t(sp) * G + g) * (D + 2) + 1) * w;
+            s_sw[sp][g] = w;
+        }
+        s_L[g] = Lg;
+    }
+    __syncthreads();
     for (int i = tid; i < G * int(head_dim); i += kThreads) {
         const int g = i / int(head_dim), d = i % int(head_dim);
-        float Mg = -CUDART_INF_F;
+        float acc = 0.0f;
+#pragma unroll 8
         for (int sp = 0; sp < nsplit; ++sp)
-            Mg = fmaxf(Mg, __ldcg(part_base + (size_t(sp) * G + g) * (D + 2)));
-        float Lg = 0.0f, acc = 0.0f;
-        for (int sp = 0; sp < nsplit; ++sp) {
-            const float* pp = part_base + (size_t(sp) * G + g) * (D + 2);
-            const float ms = __ldcg(pp);
-            if (ms == -CUDART_INF_F) continue;
-            const float w = exp2f(ms - Mg);
-            Lg += __ldcg(pp + 1) * w;
-            acc += __ldcg(pp + 2 + d) * w;
-        }
+            acc += __ldcg(part_base + (size_t(sp) * G + g) * (D + 2) + 2 + d) * s_sw[sp][g];
         const size_t oi = (size_t(b) * Hq + size_t(kvh) * G + g) * head_dim + d;
-        if (out_dtype == QK_DTYPE_F32) static_cast<float*>(out)[oi] = acc / Lg;
-        else static_cast<__half*>(out)[oi] = __float2half_rn(acc / Lg);
+        if (out_dtype == QK_DTYPE_F32) static_cast<float*>(out)[oi] = acc / s_L[g];
+        else static_cast<__half*>(out)[oi] = __float2half_rn(acc / s_L[g]);
     }
     if (tid == 0) ws_ticket[bk] = 0;  // re-arm for the next launch / graph replay
 }
@@ -342,6 +415,12 @@ template <int G>
 int run_topk(const qk_cache* c, uint32_t layer, const double* scores, uint32_t sstride,
              uint32_t batch, uint32_t k_budget, int force, int reduce, int32_t* pages,
              uint32_t pstride, int32_t* counts, cudaStream_t st) {
+    if (c->Pmax <= kRowMaxPages) {  // keys in registers (topk_rows.cuh)
+        launch_topk_rows<G>(batch * c->Hkv, c->Pmax, scores, sstride, c->d_len, layer, c->B,
+                            c->Hkv, c->S, k_budget, force, reduce, pages, pstride, counts, st);
+        const_cast<qk_cache*>(c)->launches++;
+        return cuda_check(cudaGetLastError(), "topk_rows_kernel");
+    }
     const uint32_t kpt = (c->Pmax + kSelThreads - 1) / kSelThreads;  // sized for the capacity
     const size_t smem = size_t(kSelThreads) * (kpt + 1) * sizeof(unsigned long long);
     auto kern = group_topk_kernel<G>;
@@ -359,16 +438,20 @@ template <int D, int G>
 int run_attend(const qk_cache* c, uint32_t layer, const __half* q, uint32_t batch,
                const int32_t* pages, uint32_t pstride, const int32_t* counts, uint32_t max_list,
                void* out, int out_dtype, cudaStream_t st) {
-    const uint32_t splits =
-        max_list <= uint32_t(kMinPagesPerSplit) * kMaxSplits
-            ? (max_list + kMinPagesPerSplit - 1) / kMinPagesPerSplit
-            : uint32_t(kMaxSplits);
+    // Pages per split: 8 (attend.cu's rule) unless the grid has CTAs to spare, then 16 (a
+    // CTA's fixed costs -- q fragments, combine, partials, merge ticket -- over more pages).
+    const uint32_t units = batch * c->Hkv;
+    const uint32_t s8 = (max_list + kMinPagesPerSplit - 1) / kMinPagesPerSplit;
+    const int min_pps = (uint64_t(units) * s8 >= 8u * 148u) ? 2 * kMinPagesPerSplit : kMinPagesPerSplit;
+    const uint32_t splits = max_list <= uint32_t(min_pps) * kMaxSplits
+                                ? (max_list + min_pps - 1) / min_pps
+                                : uint32_t(kMaxSplits);
     const dim3 grid(splits ? splits : 1, batch * c->Hkv);
     const float scale_log2 = float(1.4426950408889634 / sqrt(double(c->desc.head_dim)));
     grouped_attend_kernel<D, G><<<grid, kThreads, 0, st>>>(
         c->k_pool, c->v_pool, c->d_len, q, pages, pstride, counts, layer, c->B, c->Hkv, c->S,
         c->desc.head_dim, c->slice_kv, scale_log2, c->ws_partial, c->ws_ticket, out, out_dtype,
-        c->d_status);
+        c->d_status, min_pps);
     const_cast<qk_cache*>(c)->launches++;
     return cuda_check(cudaGetLastError(), "grouped_attend_kernel");
 }

@@ -11,7 +11,7 @@
 // the other K-1 picks are the best K-1 of the rest; if it is not, it is not among the
 // best K-1 either.  So the kernel selects the best `target` of the candidate pages
 // exactly (select.cuh) and appends P-1, the largest index, keeping the output ascending.
-#include "select.cuh"
+#include "topk_rows.cuh"
 
 namespace qk {
 namespace {
@@ -60,6 +60,13 @@ int launch_topk(const qk_cache* c, uint32_t layer, const double* scores, uint32_
     // Keys of up to max_pages pages per CTA; callers pass the cache capacity so that a CUDA
     // graph captured now stays in bounds when replays grow the context.
     if (max_pages < c->Pmax) max_pages = c->Pmax;
+    if (max_pages <= kRowMaxPages) {  // keys in registers (topk_rows.cuh)
+        launch_topk_rows<1>(batch * c->Hq, max_pages, scores, sstride, c->d_len, layer, c->B,
+                            c->Hq, c->S, k, cfg.force_include_recent, QK_GROUP_MAX, pages,
+                            pstride, counts, st);
+        const_cast<qk_cache*>(c)->launches++;
+        return cuda_check(cudaGetLastError(), "topk_rows_kernel");
+    }
     const uint32_t kpt = (max_pages + kThreads - 1) / kThreads;
     const size_t smem = size_t(kThreads) * (kpt + 1) * sizeof(unsigned long long);
     if (int rc = ensure_func_attrs(reinterpret_cast<const void*>(topk_kernel), smem, c->desc.device,
