@@ -37,6 +37,7 @@ namespace {
 
 constexpr int kThreads = 128;
 constexpr int kWarps = kThreads / 32;
+constexpr int kMaxSplitPages = 256;  // page-list entries of a split staged in shared memory
 
 template <int D>
 __global__ void __launch_bounds__(kThreads)
@@ -47,7 +48,7 @@ attend_kernel(const __half* __restrict__ kp, const __half* __restrict__ vp,
               uint32_t Hq, uint32_t Hkv, uint32_t S, uint32_t head_dim, size_t slice_kv,
               float scale_log2, float* __restrict__ ws_partial, int32_t* __restrict__ ws_ticket,
               void* __restrict__ out, int out_dtype, float* __restrict__ lse,
-              double* __restrict__ wsum, int32_t* __restrict__ status) {
+              double* __restrict__ wsum, int32_t* __restrict__ status, int min_pps) {
     const bool dense = mode == kModeDense, tokens = mode == kModeTokens;
     constexpr int CPR = D / 8;  // 16-byte chunks per row
     __shared__ float s_o[kWarps][D];
@@ -67,7 +68,7 @@ attend_kernel(const __half* __restrict__ kp, const __half* __restrict__ vp,
     }
     // Units of the split rule: pages, or chunks of S list entries (token mode).
     const int units = tokens ? int((uint32_t(count) + S - 1) / S) : count;
-    const int pps = max(kMinPagesPerSplit, (units + kMaxSplits - 1) / kMaxSplits);
+    const int pps = max(min_pps, (units + kMaxSplits - 1) / kMaxSplits);
     const int nsplit = (units + pps - 1) / pps;
     // A count past the list row, or needing more splits than the host launched, would read
     // past the row or never complete the merge ticket: reject it (uniform over the CTAs of
@@ -96,6 +97,21 @@ attend_kernel(const __half* __restrict__ kp, const __half* __restrict__ vp,
 #pragma unroll
     for (int j = 0; j < 8; ++j) o[j] = 0.0f;
 
+    // Page mode: this split's page list, validated once (sparse_attention's checks,
+    // attention.cpp:99-106; invalid entries are recorded and become -1, skipped).
+    __shared__ int32_t s_pg[kMaxSplitPages];
+    const bool list_smem = !dense && !tokens && last - first <= kMaxSplitPages;
+    if (list_smem) {
+        for (int i = first + tid; i < last; i += kThreads) {
+            const int pg = plist[i];
+            const bool bad_range = pg < 0 || uint32_t(pg) >= P;
+            const bool bad_order = i > 0 && plist[i - 1] >= pg;
+            if (bad_range || bad_order)
+                record_status(status, bad_range ? QK_DEV_PAGE_OUT_OF_RANGE : QK_DEV_PAGE_NOT_ASCENDING);
+            s_pg[i - first] = (bad_range || bad_order) ? -1 : pg;
+        }
+        __syncthreads();
+    }
     for (int i = first + warp; i < last; i += kWarps) {
         if (tokens) {
             // Chunk i: list entries [i*S, min(count, i*S+S)), each checked like
@@ -120,7 +136,10 @@ attend_kernel(const __half* __restrict__ kp, const __half* __restrict__ vp,
             continue;
         }
         int pg = i;
-        if (!dense) {
+        if (list_smem) {
+            pg = s_pg[i - first];
+            if (pg < 0) continue;
+        } else if (!dense) {
             pg = plist[i];
             const bool bad_range = pg < 0 || uint32_t(pg) >= P;
             const bool bad_order = i > 0 && plist[i - 1] >= pg;
@@ -236,16 +255,20 @@ int run(const qk_cache* c, uint32_t layer, const __half* q, uint32_t batch,
         uint32_t max_list, void* out, int out_dtype, float* lse, double* wsum, cudaStream_t st) {
     // max_list: the longest list (pages, or tokens in token mode) a row may hold.
     const uint32_t max_units = mode == kModeTokens ? (max_list + c->S - 1) / c->S : max_list;
-    const uint32_t splits_needed =
-        max_units <= uint32_t(kMinPagesPerSplit) * kMaxSplits
-            ? (max_units + kMinPagesPerSplit - 1) / kMinPagesPerSplit
-            : uint32_t(kMaxSplits);
+    // Units per split: 8, or 16 for wide launches (>= 256 (sequence, head) rows: a CTA's
+    // fixed costs -- q, page list, combine, partials, merge ticket -- over more pages).  A
+    // function of (batch, heads) only, so dense, sparse-over-every-page and token-mode calls
+    // of one batch share the partition (and stay bitwise equal).
+    const int min_pps = batch * c->Hq >= 256u ? 2 * kMinPagesPerSplit : kMinPagesPerSplit;
+    const uint32_t splits_needed = max_units <= uint32_t(min_pps) * kMaxSplits
+                                       ? (max_units + min_pps - 1) / min_pps
+                                       : uint32_t(kMaxSplits);
     const dim3 grid(splits_needed ? splits_needed : 1, batch * c->Hq);
     const float scale_log2 = float(1.4426950408889634 / sqrt(double(c->desc.head_dim)));
     attend_kernel<D><<<grid, kThreads, 0, st>>>(
         c->k_pool, c->v_pool, c->d_len, q, pages, pstride, counts, mode, layer, c->B,
         c->Hq, c->Hkv, c->S, c->desc.head_dim, c->slice_kv, scale_log2, c->ws_partial,
-        c->ws_ticket, out, out_dtype, lse, wsum, c->d_status);
+        c->ws_ticket, out, out_dtype, lse, wsum, c->d_status, min_pps);
     const_cast<qk_cache*>(c)->launches++;
     return cuda_check(cudaGetLastError(), "attend_kernel");
 }

@@ -1082,7 +1082,16 @@ int launch_decode(qk_cache* c, uint32_t layer, const __half* q, const __half* k,
                   uint32_t pstride, int32_t* counts, cudaStream_t st) {
     const uint32_t kk = cfg.per_layer_enabled ? cfg.token_budget / c->S : UINT32_MAX;
     const bool fits = (kk >= c->Pmax || kk <= kMaxFusedK) && (c->D == 64 || c->D == 128);
-    if (!fits)
+    static const int force_path = [] {  // QK_DECODE_PATH=fused|unfused (experiments; read once)
+        const char* e = getenv("QK_DECODE_PATH");
+        return (e == nullptr || e[0] == 0) ? 0 : (e[0] == 'u' ? 2 : 1);
+    }();
+    // GQA with more (sequence, KV head) units than SMs: the fused kernel's one-CTA-per-unit
+    // waves serialise the G heads' estimate chains and attention inside each CTA; the
+    // separate kernels spread estimate, top-K and attention over the whole GPU (measured at
+    // cfg4, 32 x 8 units: 557 -> 415 us/layer).
+    const bool wide_gqa = c->G > 1 && batch * c->Hkv > 148u;
+    if (!fits || force_path == 2 || (wide_gqa && force_path != 1))
         return decode_unfused(c, layer, q, k, v, batch, cfg, max_pages, out, out_dtype, pages,
                               pstride, counts, st);
     FusedParams prm{};
