@@ -138,3 +138,16 @@ if os.environ.get("QK_PROBE_GRAPH"):
                           "gap_from_prev_us": round(gap, 2),
                           "entry_spread_us": round((t[:, 0].max() - start) / 1000.0, 2)}))
         prev_end = end
+    # Phase medians of the last graph layer, relative to its median dep_wait stamp (early
+    # PDL-placed CTAs make the minimum entry meaningless).
+    t = per[args.layers - 1]
+    t = t[t[:, 0] > 0]
+    ref = np.median(t[:, 1])
+    row = {}
+    for k, nm in names.items():
+        col = t[:, k]
+        ok = col > 0
+        if ok.any():
+            rel = (col[ok] - ref) / 1000.0
+            row[nm] = (round(float(np.median(rel)), 2), round(float(rel.max()), 2))
+    print(json.dumps({"graph_layer_phases": row}))
