@@ -110,7 +110,7 @@ __device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
 }
 
 template <int D, int G>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, 3)
 grouped_attend_kernel(const __half* __restrict__ kp, const __half* __restrict__ vp,
                       const int32_t* __restrict__ len, const __half* __restrict__ q,
                       const int32_t* __restrict__ pages, uint32_t pstride,
@@ -306,6 +306,7 @@ grouped_attend_kernel(const __half* __restrict__ kp, const __half* __restrict__ 
             o[nt][1] = acc[1];
         }
     };
+#ifdef QK_GROUPED_DOUBLE_BUFFER
     Chunk c0, c1;  // two buffers, alternating roles (no register copies)
     load(c0);
     while (c0.n) {
@@ -315,6 +316,12 @@ grouped_attend_kernel(const __half* __restrict__ kp, const __half* __restrict__ 
         load(c0);
         fold(c1);
     }
+#else
+    // One chunk in flight per warp; occupancy (3 CTAs per SM) supplies the parallelism (the
+    // double-buffered form measured the same at cfg4 with twice the registers).
+    Chunk c0;
+    for (load(c0); c0.n; load(c0)) fold(c0);
+#endif
     // This warp's mass of head r: the four lanes of the row.
     l += __shfl_xor_sync(0xffffffffu, l, 1);
     l += __shfl_xor_sync(0xffffffffu, l, 2);
