@@ -227,3 +227,38 @@ def test_gqa_estimate_reads_shared_metadata(qk, oracle_c):
             mn, mx = oracle_c.metadata(keys[h // G], S)
             want = oracle_c.estimate_all(q[0, h], mn, mx)
             assert np.array_equal(scores[0, h, :P].view(np.uint64), want.view(np.uint64)), (G, h)
+
+
+@pytest.mark.parametrize("Hq,Hkv,B", [(32, 8, 19), (16, 8, 20), (16, 2, 75)])
+def test_wide_gqa_estimate_bitwise(qk, Hq, Hkv, B):
+    """Wide GQA launches (more (sequence, KV head) units than SMs, the shape the decode step
+    sends to the separate kernels): scores of sampled (sequence, query head) rows bitwise equal
+    to the oracle, across ragged lengths (partial page blocks, partial pages) and special
+    values (subnormals, signed zeros, +-65504)."""
+    import torch
+    from oracle import Oracle
+
+    rng = np.random.default_rng(Hq * 100 + B)
+    d, S = 128, 16
+    lens = [int(x) for x in rng.integers(300, 9000, size=B)]
+    qc = qk.QuestCache(d, S, max_batch=B, num_q_heads=Hq, num_kv_heads=Hkv, max_tokens=max(lens))
+    keys = []
+    specials = np.array([0.0, -0.0, 6e-8, -6e-8, 65504.0, -65504.0, 1e-5], np.float32)
+    for b, L in enumerate(lens):
+        k = (rng.standard_normal((Hkv, L, d)) / np.sqrt(d)).astype(np.float32)
+        mask = rng.random(k.shape) < 0.002
+        k[mask] = rng.choice(specials, size=int(mask.sum()))
+        k16 = k.astype(np.float16)
+        qc.prefill(0, b, torch.from_numpy(k16).cuda(), torch.from_numpy(k16).cuda())
+        keys.append(k16.astype(np.float32))
+    q = (rng.standard_normal((B, Hq, d)) / np.sqrt(d)).astype(np.float16)
+    q[0, 0, :4] = np.array([0.0, -0.0, 6e-8, -65504.0], np.float16)
+    scores = qc.estimate(0, torch.from_numpy(q).cuda()).cpu().numpy()
+    orc = Oracle()
+    G = Hq // Hkv
+    for b in list(range(0, B, max(1, B // 6))) + [B - 1]:
+        for h in (0, Hq - 1, int(rng.integers(0, Hq))):
+            mn, mx = orc.metadata(keys[b][h // G], S)
+            want = orc.estimate_all(q[b, h].astype(np.float32), mn, mx)
+            got = scores[b, h, : len(want)]
+            assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), (b, h)
