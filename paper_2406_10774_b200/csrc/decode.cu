@@ -259,6 +259,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
 
     // Peers store into this CTA's shared memory during the estimate: the cluster must have
     // started everywhere first (arrive now, wait just before the first remote store).
+    __syncwarp();  // thread 0's barrier set-up above: reconverge before the aligned arrive
     asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
     // Everything below reads data earlier kernels wrote.
     stamp(p.probe, 0);
