@@ -106,6 +106,9 @@ void free_cache(qk_cache* c) {
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->host_stage) cudaFreeHost(c->host_stage);
+    for (auto& hg : c->host_graphs)
+        if (hg.exec) cudaGraphExecDestroy(hg.exec);
+    if (c->capture_stream) cudaStreamDestroy(c->capture_stream);
     delete c;
 }
 
@@ -775,8 +778,8 @@ int qk_decode_step_host(qk_cache* c, uint32_t layer, const uint16_t* q_host,
         if (rc) return rc;
         void* d = nullptr;
         rc = cuda_check(cudaHostGetDevicePointer(&d, h, 0), "cudaHostGetDevicePointer");
-        if (!rc) rc = cuda_check(cudaMalloc(&c->done_counter, sizeof(uint32_t)), "cudaMalloc done");
-        if (!rc) rc = cuda_check(cudaMemset(c->done_counter, 0, sizeof(uint32_t)), "cudaMemset done");
+        if (!rc) rc = cuda_check(cudaMalloc(&c->done_counter, 2 * sizeof(uint32_t)), "cudaMalloc done");
+        if (!rc) rc = cuda_check(cudaMemset(c->done_counter, 0, 2 * sizeof(uint32_t)), "cudaMemset done");
         if (rc) {
             cudaFreeHost(h);
             return rc;
@@ -797,13 +800,19 @@ int qk_decode_step_host(qk_cache* c, uint32_t layer, const uint16_t* q_host,
     // Completion: the fused kernel's last unit publishes `seq` in the mapped word, so the host
     // spins on it (~1 us after the last output lands) instead of synchronising the stream.
     // Paths that do not consume the request (unfused fallback) synchronise as before.
-    const uint32_t seq = ++c->done_seq;
+    // The kernel publishes the device's count of completed host steps: the host expects one
+    // more than the last value it saw (advanced only when a fused launch consumed the request).
+    const uint32_t seq = c->done_seq + 1u;
     c->pending_done_flag = c->done_flag_dev;
-    c->pending_done_seq = seq;
+    if (c->host_graphs.size() != c->L) c->host_graphs.resize(c->L);
+    static const int no_graph = getenv("QK_NO_HOST_GRAPH") ? 1 : 0;  // read once
+    c->host_graph_mode = !no_graph;
     int rc = qk_decode_step(c, layer, dq, k_host ? dq + nq : nullptr, k_host ? dq + nq + nkv : nullptr,
                             batch, cfg, dout, QK_DTYPE_F32, nullptr, 0, nullptr, stream);
+    c->host_graph_mode = false;
     const bool signalled = c->pending_done_flag == nullptr;  // consumed by a fused launch
     c->pending_done_flag = nullptr;
+    if (signalled && !rc) c->done_seq = seq;
     if (!rc && signalled) {
         const volatile uint32_t* word = reinterpret_cast<volatile uint32_t*>(c->host_stage + in_max + out_max);
         const auto t0 = std::chrono::steady_clock::now();

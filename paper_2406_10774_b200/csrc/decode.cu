@@ -23,7 +23,9 @@
 // restores the full estimate_all (every page, scores kept in HBM) for parity tests.
 // The launch uses programmatic dependent launch; griddepcontrol.wait precedes every read
 // of data a prior kernel wrote.
+#include <cstring>
 #include <type_traits>
+#include <vector>
 
 #include "attend_warp.cuh"
 #include "select.cuh"
@@ -173,8 +175,8 @@ struct FusedParams {
     float scale_log2;
     unsigned long long* probe;  // optional [grid][kProbeSlots] globaltimer stamps
     uint32_t* done_flag;        // optional host-mapped completion word (host step)
-    uint32_t* done_counter;     // units finished in this launch (reset by the last one)
-    uint32_t done_seq;
+    uint32_t* done_counter;     // [0] units finished in this launch (reset by the last one),
+                                // [1] host steps completed (the value published)
 };
 
 // Host-step completion (called by thread 0 of a unit's rank-0 CTA once its outputs are
@@ -184,7 +186,11 @@ __device__ __forceinline__ void signal_done(const FusedParams& p, uint32_t units
     __threadfence_system();
     if (atomicAdd(p.done_counter, 1u) == units - 1) {
         *p.done_counter = 0;  // for the next launch (ordered by the kernel boundary)
-        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.done_flag), "r"(p.done_seq) : "memory");
+        // The sequence lives on the device (a replayed CUDA graph carries fixed parameters):
+        // the host expects one more than the last value it saw.
+        const uint32_t seq = p.done_counter[1] + 1u;
+        p.done_counter[1] = seq;
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.done_flag), "r"(seq) : "memory");
     }
 }
 
@@ -1022,10 +1028,37 @@ int run_fused(qk_cache* c, FusedParams prm, uint32_t batch, uint32_t cluster,
     attrs[1].val.programmaticStreamSerializationAllowed = pdl;
     cfg.attrs = attrs;
     cfg.numAttrs = 2;
-    const int rc = cuda_check(cudaLaunchKernelEx(&cfg, kern, prm, uint32_t(region_a)),
-                              "decode_fused_kernel");
     c->launches++;
-    return rc;
+    if (c->host_graph_mode && prm.probe == nullptr && prm.layer < c->host_graphs.size()) {
+        // Host step: replay this layer's captured launch while it is unchanged.
+        auto& hg = c->host_graphs[prm.layer];
+        std::vector<unsigned char> key(sizeof(prm) + 4 * sizeof(uint32_t));
+        const uint32_t shape[4] = {cfg.gridDim.x, cluster, uint32_t(smem), uint32_t(region_a)};
+        std::memcpy(key.data(), &prm, sizeof(prm));
+        std::memcpy(key.data() + sizeof(prm), shape, sizeof(shape));
+        if (hg.exec == nullptr || hg.key != key) {
+            if (hg.exec) cudaGraphExecDestroy(hg.exec);
+            hg.exec = nullptr;
+            if (!c->capture_stream)
+                if (int rc = cuda_check(cudaStreamCreateWithFlags(&c->capture_stream, cudaStreamNonBlocking),
+                                        "capture stream"))
+                    return rc;
+            cudaGraph_t g = nullptr;
+            cfg.stream = c->capture_stream;
+            if (int rc = cuda_check(cudaStreamBeginCapture(c->capture_stream, cudaStreamCaptureModeThreadLocal),
+                                    "host-step capture"))
+                return rc;
+            const cudaError_t le = cudaLaunchKernelEx(&cfg, kern, prm, uint32_t(region_a));
+            const cudaError_t ee = cudaStreamEndCapture(c->capture_stream, &g);
+            if (int rc = cuda_check(le != cudaSuccess ? le : ee, "host-step capture")) return rc;
+            const cudaError_t ie = cudaGraphInstantiate(&hg.exec, g, 0);
+            cudaGraphDestroy(g);
+            if (int rc = cuda_check(ie, "host-step graph instantiate")) return rc;
+            hg.key = std::move(key);
+        }
+        return cuda_check(cudaGraphLaunch(hg.exec, st), "decode_fused_kernel (graph)");
+    }
+    return cuda_check(cudaLaunchKernelEx(&cfg, kern, prm, uint32_t(region_a)), "decode_fused_kernel");
 }
 
 template <int D>
@@ -1095,7 +1128,8 @@ int launch_decode(qk_cache* c, uint32_t layer, const __half* q, const __half* k,
     if (!fits || force_path == 2 || (wide_gqa && force_path != 1))
         return decode_unfused(c, layer, q, k, v, batch, cfg, max_pages, out, out_dtype, pages,
                               pstride, counts, st);
-    FusedParams prm{};
+    FusedParams prm;
+    std::memset(&prm, 0, sizeof(prm));  // padding too: the host step keys its graphs on the bytes
     prm.k_pool = c->k_pool;
     prm.v_pool = c->v_pool;
     prm.meta = c->meta;
@@ -1132,7 +1166,6 @@ int launch_decode(qk_cache* c, uint32_t layer, const __half* q, const __half* k,
     if (c->pending_done_flag) {  // the host step asked for a completion word (consumed here)
         prm.done_flag = c->pending_done_flag;
         prm.done_counter = c->done_counter;
-        prm.done_seq = c->pending_done_seq;
         c->pending_done_flag = nullptr;
     }
     const uint32_t cluster = fused_cluster_size(c, batch, max_pages);

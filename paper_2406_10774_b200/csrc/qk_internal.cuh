@@ -81,12 +81,23 @@ struct qk_cache {
     unsigned char* host_stage_dev = nullptr;  // (q, k, v in; fp32 out), allocated lazily
     // Host-step completion: the last unit of a fused launch writes `seq` into the mapped word
     // (the host spins on it instead of a stream synchronisation).
-    uint32_t* done_counter = nullptr;    // device: units finished in the current launch
+    uint32_t* done_counter = nullptr;    // device [2]: units finished in the current launch,
+                                         // completed host steps (the published sequence)
     uint32_t* done_flag_dev = nullptr;   // device view of the mapped completion word
     uint32_t done_seq = 0;
     uint32_t* pending_done_flag = nullptr;  // set by the host step for the next fused launch;
-    uint32_t pending_done_seq = 0;          // launch_decode clears it when it consumes it
+                                            // launch_decode clears it when it consumes it
     unsigned long long* probe = nullptr; // phase timestamps of the fused kernel (QK_PROBE)
+    // Host step: one instantiated CUDA graph per layer holding its fused launch, replayed while
+    // the launch (parameters, grid, cluster, shared memory) is unchanged -- a graph launch costs
+    // ~1.5 us less host-to-GPU round trip than cudaLaunchKernelEx with cluster attributes.
+    struct HostGraph {
+        cudaGraphExec_t exec = nullptr;
+        std::vector<unsigned char> key;  // bytes of the launch it replays
+    };
+    std::vector<HostGraph> host_graphs;  // [L]
+    cudaStream_t capture_stream = nullptr;
+    bool host_graph_mode = false;        // set by qk_decode_step_host around its launch
     bool keep_scores = false;            // fused step: estimate every page, keep scores
     uint64_t device_bytes = 0;
     std::atomic<uint64_t> launches{0};
