@@ -10,6 +10,7 @@
 //   F  128 CTAs, L2 prefetch (cp.async.bulk.prefetch.L2) of every row first, then A's loads
 // Prints the launch time (CUDA events) and the implied TB/s.
 #include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -118,6 +119,14 @@ __global__ void __launch_bounds__(512, 1) prefetch_then_load(const __half* meta,
 
 __global__ void empty_kernel(int* sink) { T_START T_END }
 
+__global__ void touch_pages(const char* __restrict__ p, size_t n, int* sink) {
+    int acc = 0;
+    for (size_t i = (blockIdx.x * size_t(blockDim.x) + threadIdx.x) * 65536; i < n;
+         i += size_t(gridDim.x) * blockDim.x * 65536)
+        acc ^= __ldcg(reinterpret_cast<const int*>(p + i));
+    if (acc == 0x12345678) sink[0] = acc;
+}
+
 __global__ void flush(const int4* p, size_t n, int* sink) {
     int acc = 0;
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
@@ -130,7 +139,7 @@ int main() {
     __half* meta;
     int* sink;
     int4* junk;
-    const size_t junk_n = (size_t(192) << 20) / 16;  // > L2, < TLB reach with meta
+    const size_t junk_n = (size_t(getenv("BIGFLUSH") ? 4096 : 192) << 20) / 16;  // BIGFLUSH: TLB thrash
     cudaMalloc(&meta, meta_elems * 2);
     cudaMemset(meta, 1, meta_elems * 2);
     cudaMalloc(&sink, 4096);
@@ -144,7 +153,8 @@ int main() {
     auto run = [&](const char* name, auto launch, int grid) {
         float best = 1e9f, sum = 0, dbest = 1e9f;
         for (int rep = 0; rep < 12; ++rep) {
-            flush<<<592, 512>>>(junk, junk_n, sink);
+            if (getenv("BIGFLUSH")) touch_pages<<<148, 512>>>(reinterpret_cast<const char*>(junk), junk_n * 16, sink);
+            flush<<<592, 512>>>(junk, getenv("BIGFLUSH") ? (size_t(192) << 20) / 16 : junk_n, sink);
             cudaEventRecord(a);
             launch();
             cudaEventRecord(b);
