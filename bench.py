@@ -361,11 +361,19 @@ def run_ours(args):
     from paper_2406_10774_b200.shard import gather_outputs, partition
 
     rank, world, local = dist_env()
+    # QK_BENCH_BACKEND=gloo: a code-path check of N > 1 on a one-GPU rig (ranks share the
+    # device modulo the device count; the numbers are not scaling measurements).
+    backend = os.environ.get("QK_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    coll_dev = dev if backend == "nccl" else torch.device("cpu")  # gloo: host tensors
     w = Workload(args, world)
     HQ, HKV, B, NL, ctx, budget = w.HQ, w.HKV, w.B, w.NL, w.ctx, w.budget
     G = HQ // HKV
@@ -453,7 +461,7 @@ def run_ours(args):
     qc.sync_lengths(stream=stream)  # graph replays advanced only the device lengths
     qc.check_status(stream=stream)
     if world > 1:
-        t = torch.tensor([elapsed_ms], device=dev)
+        t = torch.tensor([elapsed_ms], device=coll_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed_ms = float(t.item())
     ms_per_step = elapsed_ms / args.steps
@@ -555,7 +563,7 @@ def run_ours(args):
                     "host memory, the step, D2H of the fp32 output")
         d2h = HQ * B * HEAD_DIM * 4 * NL
     if world > 1:
-        t = torch.tensor([e2e_s], device=dev)
+        t = torch.tensor([e2e_s], device=coll_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e_us = e2e_s * 1e6 / (e2e_steps * NL)
@@ -571,7 +579,7 @@ def run_ours(args):
                         "per layer, 8 layers x 20 steps; host q/k/v in, fp32 out to host")
     h2d = (lq + 2 * lkv) * lb * HEAD_DIM * 2 * NL  # q, k, v fp16 per layer
 
-    per_gpu = torch.tensor([own_us_per_layer], device=dev)
+    per_gpu = torch.tensor([own_us_per_layer], device=coll_dev)
     if world > 1:
         gathered = [torch.zeros_like(per_gpu) for _ in range(world)]
         dist.all_gather(gathered, per_gpu)
