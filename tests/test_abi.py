@@ -105,3 +105,20 @@ def test_null_handles_are_rejected():
     assert lib.qk_append(None, 0, None, None, 1, None) == _lib.QK_ERR_INVALID_ARGUMENT
     assert lib.qk_estimate(None, 0, None, 1, None, 0, None) == _lib.QK_ERR_INVALID_ARGUMENT
     assert lib.qk_cache_destroy(None) == _lib.QK_OK
+
+
+def test_grouped_entry_points_reject_null_handles():
+    """The GQA group-shared entry points validate before touching a device."""
+    from paper_2406_10774_b200 import _lib
+
+    lib = _lib.load()
+    cfg = _lib.qk_selection_cfg(256, 1, 1)
+    assert lib.qk_select_topk_grouped(None, 0, None, 0, 1, ctypes.byref(cfg), _lib.QK_GROUP_MAX,
+                                      None, 0, None, None) == _lib.QK_ERR_INVALID_ARGUMENT
+    assert "null argument" in lib.qk_last_error().decode()
+    assert lib.qk_sparse_attend_grouped(None, 0, None, 1, None, 0, None, None, 0,
+                                        None) == _lib.QK_ERR_INVALID_ARGUMENT
+    assert lib.qk_decode_step_grouped(None, 0, None, None, None, 1, ctypes.byref(cfg),
+                                      _lib.QK_GROUP_SUM, None, 0, None, 0, None,
+                                      None) == _lib.QK_ERR_INVALID_ARGUMENT
+    assert (_lib.QK_GROUP_MAX, _lib.QK_GROUP_SUM) == (1, 2)

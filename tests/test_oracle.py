@@ -251,3 +251,30 @@ def test_oracle_matches_reference_random(oracle_c, reference):
         assert np.array_equal(s_ref.view(np.uint64), s_or.view(np.uint64))
         assert p_ref.tolist() == p_or.tolist()
         assert np.array_equal(o_ref, o_or)
+
+
+def test_group_quest_step_composes_the_reference(oracle_c, reference):
+    """The checker of the GQA group-shared variant (Oracle.group_quest_step) equals the same
+    composition of the unmodified reference's functions: per-head estimate_all, the group
+    score (max / fp64 sum in head order), one select_top_k, each head's sparse_attention."""
+    rng = np.random.default_rng(17)
+    for trial in range(12):
+        d, S, G = int(rng.choice([16, 64, 128])), int(rng.choice([4, 16])), int(rng.choice([2, 4, 8]))
+        L = int(rng.integers(S, 500))
+        sd = 1 / np.sqrt(d)
+        k, v = half(rng.standard_normal((L, d)) * sd), half(rng.standard_normal((L, d)) * sd)
+        qs = half(rng.standard_normal((G, d)) * sd)
+        budget = int(rng.integers(S, 8 * S + 1))
+        reduce = "max" if trial % 2 else "sum"
+        force = bool(trial % 3)
+        group, pages, outs = oracle_c.group_quest_step(qs, k, v, S, budget, reduce, force)
+        per_head = [reference.estimate_all(q, k, S) for q in qs]
+        want = per_head[0].copy()
+        for s_ in per_head[1:]:
+            want = np.maximum(want, s_) if reduce == "max" else want + s_
+        assert np.array_equal(group.view(np.uint64), want.view(np.uint64)), trial
+        ref_pages = reference.select_top_k(want, S, budget, force)
+        assert pages.tolist() == ref_pages.tolist(), trial
+        for g in range(G):
+            ref_out, _ = reference.sparse_attention(qs[g], k, v, S, ref_pages)
+            assert np.array_equal(outs[g], ref_out), (trial, g)
