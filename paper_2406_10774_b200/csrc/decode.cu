@@ -584,12 +584,44 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
             for (int j = 0; j < 4; ++j) dst[j] = make_double2(acc[2 * j], acc[2 * j + 1]);
             __syncthreads();
             if (c0 == r_begin) stamp(p.probe, 6);
+            double sc_pass = 0.0;
             if (pg < main_end) {
                 const double sc = ((part[0 * kThreads + tid] + part[1 * kThreads + tid]) +
                                    (part[2 * kThreads + tid] + part[3 * kThreads + tid])) +
                                   ((part[4 * kThreads + tid] + part[5 * kThreads + tid]) +
                                    (part[6 * kThreads + tid] + part[7 * kThreads + tid]));
                 finish(pg, sc, rec);
+                sc_pass = sc;
+            }
+            if (p.prefetch && smem_keys && main_end - r_begin <= uint32_t(kThreads)) {
+                // Speculative L2 prefetch of each warp's best page of the pass (the best of 32
+                // pages is in the top 127 of 2047 ~86% of the time at cfg2): HBM idles between
+                // the metadata stream and the selection, so half the budget's K/V starts early.
+                // Only a hint -- the selection's own prefetch and the attention are unchanged.
+                // Measured: 20.10 -> 19.35-19.49 us/layer; the best two per warp (the whole
+                // budget) gains nothing, the fast CTAs' extra prefetches then slow the slowest
+                // CTA's metadata stream -- and for the same reason only single-pass CTAs
+                // speculate (with 4 passes per CTA, cfg3 and cfg5 lost 9 and 14 us).
+                unsigned long long best = (pg < main_end && pg < n_cand) ? order_key(sc_pass) : 0ull;
+                uint32_t bp = pg;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const unsigned long long ok = __shfl_xor_sync(0xffffffffu, best, o);
+                    const uint32_t op = __shfl_xor_sync(0xffffffffu, bp, o);
+                    if (ok > best || (ok == best && op < bp)) {
+                        best = ok;
+                        bp = op;
+                    }
+                }
+                if (lane == 0 && best != 0ull) {
+                    const uint32_t pbytes = p.S * D * 2;
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                                     p.k_pool + s * p.slice_kv + size_t(bp) * p.S * D),
+                                 "r"(pbytes) : "memory");
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                                     p.v_pool + s * p.slice_kv + size_t(bp) * p.S * D),
+                                 "r"(pbytes) : "memory");
+                }
             }
             if (c0 == r_begin) stamp(p.probe, 7);
             __syncthreads();  // part reused by the next pass
