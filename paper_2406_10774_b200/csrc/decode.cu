@@ -391,6 +391,8 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
     const bool patch = owner && new_page < n_est;  // staged copy to patch
     __shared__ __half s_new_min[D], s_new_max[D];
     __shared__ uint32_t s_rec_scratch[D / 32];
+    __shared__ uint32_t s_spec_pg[kWarps];  // each warp's speculatively prefetched page (or ~0u)
+    if (tid < kWarps) s_spec_pg[tid] = 0xffffffffu;  // (ordered by the barriers below)
     bool appended = false, arrived = false;
     // Each CTA arrives once on every CTA's keys_bar; with release when it wrote data its
     // peers read (the owner's new K/V row, scores through HBM).
@@ -613,6 +615,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
                         bp = op;
                     }
                 }
+                if (lane == 0) s_spec_pg[warp] = best != 0ull ? bp : 0xffffffffu;
                 if (lane == 0 && best != 0ull) {
                     const uint32_t pbytes = p.S * D * 2;
                     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
@@ -812,16 +815,24 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
                     const uint32_t page_bytes = p.S * D * 2;
                     const __half* kslice0 = p.k_pool + s * p.slice_kv;
                     const __half* vslice0 = p.v_pool + s * p.slice_kv;
-                    for (uint32_t i = rank + C * uint32_t(tid - NTS); i <= n_cand;
-                         i += C * uint32_t(kThreads - NTS)) {
+                    // Each CTA prefetches the proven pages of its own estimate range (and the last
+                    // CTA the newest page), skipping the pages its warps already prefetched
+                    // speculatively: fewer bulk prefetches serialised in the copy engine ahead
+                    // of the post-selection barrier.
+                    const uint32_t lo = min(r_begin, n_cand), hi = min(r_end, n_cand);
+                    const bool last = rank == C - 1;
+                    for (uint32_t i = lo + uint32_t(tid - NTS); i < hi + (last ? 1u : 0u);
+                         i += uint32_t(kThreads - NTS)) {
                         bool take;
                         uint32_t pg = i;
-                        if (i == n_cand) {
+                        if (i >= hi) {
                             take = p.force != 0 && p.prefetch;  // the newest page
                             pg = P - 1;
                         } else {
                             const unsigned long long k = keys[key_slot(i)];
                             take = ok && unsigned(((k << shift) >> 32) >> 21) > bin;
+                            const uint32_t blk = (i - r_begin) >> 5;
+                            if (take && blk < uint32_t(kWarps) && s_spec_pg[blk] == i) take = false;
                         }
                         if (!take) continue;
                         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(kslice0 + size_t(pg) * p.S * D),
