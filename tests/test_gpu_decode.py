@@ -284,3 +284,26 @@ def test_fused_selection_heavy_ties(qk, oracle_c, Hq, Hkv, L, budget):
     out = layer.qc.decode_step(0, t(q), t(kn), t(vn), budget, pages=pages, counts=counts)
     layer.qc.check_status()
     layer.check(oracle_c, q, out.cpu().numpy(), pages.cpu().numpy(), counts.cpu().numpy(), budget)
+
+
+@pytest.mark.parametrize("seed", range(32))
+def test_fused_step_random_geometry(qk, oracle_c, seed):
+    """Seeded random sweep over the fused step's geometry: batch, GQA group, head_dim
+    (including padded ones), page size, ragged lengths, budget, forced page, score retention
+    and two consecutive steps.  Pages bitwise, outputs within 1e-5 relative L2."""
+    rng = np.random.default_rng(1000 + seed)
+    B = int(rng.integers(1, 4))
+    Hkv = int(rng.choice([1, 2, 4]))
+    G = int(rng.choice([1, 2, 4, 8]))
+    d = int(rng.choice([64, 80, 96, 128, 128, 200, 256]))  # >128: the unfused route
+    S = int(rng.choice([1, 4, 8, 16, 16, 16, 32, 64]))
+    max_len = 4000 if S == 1 else 24000
+    lens = [int(x) for x in rng.integers(1, max_len, size=B)]
+    P = max(lens) // S + 2
+    budget = S * int(rng.integers(1, P + 4))
+    force = bool(rng.integers(0, 4) > 0)
+    keep = bool(rng.integers(0, 2))
+    layer = Layer(qk, rng, B, Hkv * G, Hkv, d, S, lens, keep_scores=keep)
+    for _ in range(2):
+        q, out, pages, counts = layer.step(rng, budget, force)
+        layer.check(oracle_c, q, out, pages, counts, budget, force)

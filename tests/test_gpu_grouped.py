@@ -228,3 +228,37 @@ def test_grouped_graph_replay_grows_the_context(qk):
             check_step(orc, qc, keys, vals, qh, pages, counts, out, S, budget, "max")
     qc.sync_lengths()
     assert qc.token_count(0, 0) == L0 + steps
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_grouped_step_random_geometry(qk, seed):
+    """Seeded random sweep: batch, group, head_dim (padded ones too), page size, ragged
+    lengths, budget, reduction and forced page.  Pages bitwise, outputs 1e-5 relative L2."""
+    from oracle import Oracle
+
+    rng = np.random.default_rng(5000 + seed)
+    B = int(rng.integers(1, 4))
+    Hkv = int(rng.choice([1, 2, 4]))
+    G = int(rng.choice([1, 2, 4, 8]))
+    d = int(rng.choice([64, 80, 96, 128]))
+    S = int(rng.choice([4, 8, 16, 16, 32, 64]))
+    lens = [int(x) for x in rng.integers(1, 12000, size=B)]
+    P = max((L + 1 + S - 1) // S for L in lens)
+    budget = S * int(rng.integers(1, P + 4))
+    reduce = str(rng.choice(["max", "sum"]))
+    force = bool(rng.integers(0, 4) > 0)
+    Hq = Hkv * G
+    qc, keys, vals = make(qk, rng, B, Hq, Hkv, d, S, lens)
+    sd = 1 / np.sqrt(d)
+    q = half(rng.standard_normal((B, Hq, d)) * sd)
+    kn = half(rng.standard_normal((B, Hkv, d)) * sd)
+    vn = half(rng.standard_normal((B, Hkv, d)) * sd)
+    for b in range(B):
+        keys[b] = np.concatenate([keys[b], kn[b][:, None]], axis=1)
+        vals[b] = np.concatenate([vals[b], vn[b][:, None]], axis=1)
+    pages = torch.full((B, Hkv, P), -1, dtype=torch.int32, device="cuda")
+    counts = torch.zeros((B, Hkv), dtype=torch.int32, device="cuda")
+    out = qc.decode_step_grouped(0, dev16(q), dev16(kn), dev16(vn), budget, reduce, force,
+                                 pages=pages, counts=counts)
+    qc.check_status()
+    check_step(Oracle(), qc, keys, vals, q, pages, counts, out, S, budget, reduce, force)
