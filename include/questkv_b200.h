@@ -103,6 +103,13 @@ QK_API int qk_cache_describe(const qk_cache *cache, qk_cache_desc *out);
 QK_API uint64_t qk_cache_device_bytes(const qk_cache *cache);
 /* Logical pages per cache slice the pools are sized for (ceil(max_tokens/page_size)). */
 QK_API uint32_t qk_cache_max_pages(const qk_cache *cache);
+/* Grow every slice to hold max_tokens tokens (the reference's KvCache grows page by page,
+ * kv_store.cpp:24-29): reallocates the pools, metadata and page-sized workspaces and copies
+ * the cached pages, metadata and lengths into them.  Device-synchronising; a smaller or equal
+ * max_tokens is a no-op.  Pointers captured before the call (CUDA graphs recorded by the
+ * caller) refer to the old pools and must be re-captured.  More than 16384 pages per slice
+ * -> QK_ERR_UNSUPPORTED; out of memory -> QK_ERR_CUDA with the cache unchanged. */
+QK_API int qk_cache_reserve(qk_cache *cache, uint32_t max_tokens);
 
 /* KvCache::token_count / page_count (kv_store.hpp:57-58) of one slice (all KV heads of a
  * sequence share it).  Host-side, never blocks. */

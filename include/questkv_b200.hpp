@@ -11,7 +11,9 @@
 //   * storage is fp16: keys/values/queries are rounded to fp16 (round-to-nearest-even) on
 //     the way in; for fp16-representable inputs every result equals the reference's
 //     (metadata, scores and page sets bitwise, outputs within 1e-5 relative L2);
-//   * KvCache has a fixed capacity (constructor argument; the reference grows without bound);
+//   * KvCache's constructor takes an initial capacity; appends past it grow the cache by
+//     doubling (qk_cache_reserve: a device copy) up to 16384 pages, as the reference grows
+//     its page vector;
 //   * accessors return values instead of references into host-side storage;
 //   * AttentionOutput::weights_sum_check is the post-softmax mass of the weights the kernel
 //     applied, evaluated in fp64 from its fp32 partials (1 up to fp32 rounding);
@@ -154,6 +156,7 @@ public:
         if (key.size() != config_.head_dim || value.size() != config_.head_dim)
             throw std::invalid_argument("KvCache::append: vector dimension mismatch");
         const uint32_t t = token_count();
+        ensure(uint64_t(t) + 1);
         const auto k = to_half(key), v = to_half(value);
         check(qk_append_host(cache_, 0, k.data(), v.data(), 1, nullptr));
         return t;
@@ -162,6 +165,7 @@ public:
     void extend(std::span<const float> keys, std::span<const float> values) {
         if (keys.size() != values.size() || keys.size() % config_.head_dim != 0)
             throw std::invalid_argument("KvCache::extend: shape mismatch");
+        ensure(uint64_t(token_count()) + keys.size() / config_.head_dim);
         const auto k = to_half(keys), v = to_half(values);
         check(qk_prefill_host(cache_, 0, 0, k.data(), v.data(),
                               uint32_t(keys.size() / config_.head_dim), nullptr));
@@ -210,6 +214,15 @@ public:
     qk_cache* handle() const noexcept { return cache_; }
 
 private:
+    // Grows the slice (doubling) so that `tokens` fit: the reference's page vector growth.
+    void ensure(uint64_t tokens) {
+        qk_cache_desc d{};
+        check(qk_cache_describe(cache_, &d));
+        if (tokens <= d.max_tokens) return;
+        const uint64_t cap = uint64_t(16384) * d.page_size;  // the ABI's page limit per slice
+        const uint64_t want = std::max<uint64_t>(tokens, std::min<uint64_t>(2 * uint64_t(d.max_tokens), cap));
+        check(qk_cache_reserve(cache_, uint32_t(std::min<uint64_t>(want, UINT32_MAX))));
+    }
     std::vector<float> row(uint32_t token, bool want_key) const {
         if (token >= token_count()) throw std::out_of_range("KvCache::key: token out of range");
         std::vector<uint16_t> k(config_.head_dim), v(config_.head_dim);
@@ -455,6 +468,8 @@ public:
                       uint32_t n_tokens, void* stream = nullptr) {
         check(qk_prefill_host(cache_, layer, seq, k, v, n_tokens, stream));
     }
+    // Grow every slice to max_tokens (qk_cache_reserve; device copy, graphs re-captured).
+    void reserve(uint32_t max_tokens) { check(qk_cache_reserve(cache_, max_tokens)); }
 
 private:
     qk_cache* cache_ = nullptr;

@@ -63,6 +63,7 @@ SIGNATURES = {
     "qk_cache_describe": (ctypes.c_int, [_P, ctypes.POINTER(qk_cache_desc)]),
     "qk_cache_device_bytes": (ctypes.c_uint64, [_P]),
     "qk_cache_max_pages": (ctypes.c_uint32, [_P]),
+    "qk_cache_reserve": (ctypes.c_int, [_P, ctypes.c_uint32]),
     "qk_token_count": (ctypes.c_int, [_P, _U32, _U32, ctypes.POINTER(_U32)]),
     "qk_page_count": (ctypes.c_int, [_P, _U32, _U32, ctypes.POINTER(_U32)]),
     "qk_reset": (ctypes.c_int, [_P, _U32, _P]),

@@ -215,6 +215,82 @@ int qk_cache_describe(const qk_cache* c, qk_cache_desc* out) {
     return QK_OK;
 }
 
+int qk_cache_reserve(qk_cache* c, uint32_t max_tokens) {
+    if (!c) return set_error(QK_ERR_INVALID_ARGUMENT, "qk_cache_reserve: null cache");
+    if (max_tokens <= c->desc.max_tokens) return QK_OK;
+    const uint64_t pmax = (uint64_t(max_tokens) + c->S - 1) / c->S;
+    if (pmax > kMaxPages)
+        return set_error(QK_ERR_UNSUPPORTED, "qk_cache_reserve: more than 16384 pages per slice");
+    DeviceGuard guard(c->desc.device);
+    if (int rc = cuda_check(cudaDeviceSynchronize(), "qk_cache_reserve")) return rc;
+    if (uint32_t(pmax) == c->Pmax) {  // the last page already has room
+        c->desc.max_tokens = max_tokens;
+        return QK_OK;
+    }
+    const uint32_t Pn = uint32_t(pmax);
+    const uint32_t Mn = (Pn + kMetaAlign - 1) / kMetaAlign * kMetaAlign;
+    const size_t kv_n = size_t(Pn) * c->S * c->D, meta_n = size_t(2) * c->D * Mn;
+    const size_t slices = size_t(c->L) * c->B * c->Hkv;
+    const size_t ws_n = size_t(c->B) * c->Hq * Pn;
+    // New buffers, zero-filled like qk_cache_create's; on failure the cache is untouched.
+    struct Buf {
+        void** slot;
+        size_t bytes;
+        void* p;
+    } bufs[] = {{reinterpret_cast<void**>(&c->k_pool), slices * kv_n * 2, nullptr},
+                {reinterpret_cast<void**>(&c->v_pool), slices * kv_n * 2, nullptr},
+                {reinterpret_cast<void**>(&c->meta), slices * meta_n * 2, nullptr},
+                {reinterpret_cast<void**>(&c->prange), slices * Mn * 4, nullptr},
+                {reinterpret_cast<void**>(&c->ws_scores), ws_n * 8, nullptr},
+                {reinterpret_cast<void**>(&c->ws_pages), ws_n * 4, nullptr}};
+    int rc = QK_OK;
+    for (Buf& b : bufs) {
+        if (!rc) rc = cuda_check(cudaMalloc(&b.p, b.bytes), "qk_cache_reserve: cudaMalloc");
+        if (!rc) rc = cuda_check(cudaMemset(b.p, 0, b.bytes), "qk_cache_reserve: cudaMemset");
+    }
+    // Per slice: the cached pages ([Pmax][S][D] contiguous), every metadata row ([2][D] rows
+    // of Mrow pages) and the page records keep their offsets inside the longer rows.
+    if (!rc) rc = cuda_check(cudaMemcpy2D(bufs[0].p, kv_n * 2, c->k_pool, c->slice_kv * 2,
+                                          c->slice_kv * 2, slices, cudaMemcpyDeviceToDevice),
+                             "qk_cache_reserve: copy K");
+    if (!rc) rc = cuda_check(cudaMemcpy2D(bufs[1].p, kv_n * 2, c->v_pool, c->slice_kv * 2,
+                                          c->slice_kv * 2, slices, cudaMemcpyDeviceToDevice),
+                             "qk_cache_reserve: copy V");
+    if (!rc) rc = cuda_check(cudaMemcpy2D(bufs[2].p, size_t(Mn) * 2, c->meta, size_t(c->Mrow) * 2,
+                                          size_t(c->Mrow) * 2, slices * 2 * c->D,
+                                          cudaMemcpyDeviceToDevice),
+                             "qk_cache_reserve: copy metadata");
+    if (!rc) rc = cuda_check(cudaMemcpy2D(bufs[3].p, size_t(Mn) * 4, c->prange, size_t(c->Mrow) * 4,
+                                          size_t(c->Mrow) * 4, slices, cudaMemcpyDeviceToDevice),
+                             "qk_cache_reserve: copy page records");
+    if (!rc) rc = cuda_check(cudaDeviceSynchronize(), "qk_cache_reserve");
+    if (rc) {
+        for (Buf& b : bufs)
+            if (b.p) cudaFree(b.p);
+        return rc;
+    }
+    for (Buf& b : bufs) {
+        cudaFree(*b.slot);
+        *b.slot = b.p;
+    }
+    c->device_bytes += (bufs[0].bytes + bufs[1].bytes + bufs[2].bytes + bufs[3].bytes +
+                        bufs[4].bytes + bufs[5].bytes) -
+                       (slices * (2 * c->slice_kv * 2 + c->slice_meta * 2 + size_t(c->Mrow) * 4) +
+                        size_t(c->B) * c->Hq * c->Pmax * 12);
+    c->desc.max_tokens = max_tokens;
+    c->Pmax = Pn;
+    c->Mrow = Mn;
+    c->slice_kv = kv_n;
+    c->slice_meta = meta_n;
+    // The host step's graphs hold the old pool pointers.
+    for (auto& hg : c->host_graphs) {
+        if (hg.exec) cudaGraphExecDestroy(hg.exec);
+        hg.exec = nullptr;
+        hg.key.clear();
+    }
+    return QK_OK;
+}
+
 uint64_t qk_cache_device_bytes(const qk_cache* c) { return c ? c->device_bytes : 0; }
 uint32_t qk_cache_max_pages(const qk_cache* c) { return c ? c->Pmax : 0; }
 uint64_t qk_kernel_launches(const qk_cache* c) { return c ? c->launches.load() : 0; }

@@ -96,6 +96,13 @@ class QuestCache:
         self.device = torch.device("cuda", device)
         self.max_pages = int(self._lib.qk_cache_max_pages(self._h))
 
+    def reserve(self, max_tokens: int) -> None:
+        """Grow every slice to hold ``max_tokens`` tokens (qk_cache_reserve): the cached pages,
+        metadata and lengths are kept.  Graphs captured before the call must be re-captured."""
+        check(self._lib.qk_cache_reserve(self._h, int(max_tokens)))
+        self.max_tokens = max(self.max_tokens, int(max_tokens))
+        self.max_pages = int(self._lib.qk_cache_max_pages(self._h))
+
     def close(self) -> None:
         if getattr(self, "_h", None):
             self._lib.qk_cache_destroy(self._h)
@@ -515,7 +522,8 @@ def _as_half_row(x, dim: int, what: str) -> np.ndarray:
 class KvCache:
     """questkv::KvCache (kv_store.hpp:41-65): one head's paged cache, held on the GPU.
 
-    ``capacity`` bounds the token count (the reference grows without bound).
+    ``capacity`` is the initial allocation; like the reference's page vector it grows
+    (doubling, qk_cache_reserve) when an append or extend needs more.
     """
 
     def __init__(self, config: CacheConfig, capacity: int = 8192, device: Optional[int] = None):
@@ -543,6 +551,7 @@ class KvCache:
         k = _as_half_row(key, d, "KvCache::append")
         v = _as_half_row(value, d, "KvCache::append")
         t = self.token_count()
+        self._ensure(t + 1)
         dev = self._qc.device
         self._qc.append(0, torch.from_numpy(k).to(dev).view(1, 1, d),
                         torch.from_numpy(v).to(dev).view(1, 1, d))
@@ -555,9 +564,15 @@ class KvCache:
         v = np.asarray(values, dtype=np.float32).reshape(-1, d).astype(np.float16)
         if k.shape != v.shape:
             raise ValueError("KvCache::extend: keys/values shape mismatch")
+        self._ensure(self.token_count() + k.shape[0])
         dev = self._qc.device
         self._qc.prefill(0, 0, torch.from_numpy(k).to(dev).view(1, -1, d),
                          torch.from_numpy(v).to(dev).view(1, -1, d))
+
+    def _ensure(self, tokens: int) -> None:
+        if tokens > self._qc.max_tokens:
+            cap = 16384 * self._config.page_size  # the ABI's page limit per slice
+            self._qc.reserve(max(tokens, min(2 * self._qc.max_tokens, cap)))
 
     def page_metadata(self, page_index: int) -> PageMetadata:
         """kv_store.cpp:49-54 (IndexError == std::out_of_range)."""

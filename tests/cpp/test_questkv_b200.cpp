@@ -95,6 +95,22 @@ static void kv_store_cases() {
         const float k3[3] = {1, 2, 3};
         p.append(k3, k3);
     }));
+    // Growth past the initial capacity (the reference's page vector grows on demand,
+    // kv_store.cpp:24-29): 4 -> 8 -> 16 -> 32 tokens, pages and metadata kept.
+    qk::KvCache g(qk::CacheConfig{2, 4, 2}, 4);
+    for (int t = 0; t < 23; ++t) {
+        const float k[2] = {float(t), float(100 - 3 * t)};
+        g.append(k, v);
+    }
+    std::vector<float> ks(2 * 10), vs(2 * 10, 0.5f);
+    for (int t = 0; t < 10; ++t) ks[2 * t] = ks[2 * t + 1] = float(-t);
+    g.extend(ks, vs);
+    CHECK(g.token_count() == 33 && g.page_count() == 9);
+    CHECK(g.key(22)[0] == 22.0f && g.key(22)[1] == 34.0f && g.key(32)[0] == -9.0f);
+    const qk::PageMetadata gm = g.page_metadata(1);  // tokens 4..7
+    CHECK(gm.min_key[0] == 4 && gm.max_key[0] == 7 && gm.min_key[1] == 79 && gm.max_key[1] == 88);
+    const qk::PageMetadata gm5 = g.page_metadata(5);  // tokens 20..22 appended, 23 extended
+    CHECK(gm5.min_key[0] == 0 && gm5.max_key[0] == 22 && gm5.min_key[1] == 0 && gm5.max_key[1] == 40);
 }
 
 static void criticality_cases() {

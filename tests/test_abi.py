@@ -105,6 +105,7 @@ def test_null_handles_are_rejected():
     assert lib.qk_append(None, 0, None, None, 1, None) == _lib.QK_ERR_INVALID_ARGUMENT
     assert lib.qk_estimate(None, 0, None, 1, None, 0, None) == _lib.QK_ERR_INVALID_ARGUMENT
     assert lib.qk_cache_destroy(None) == _lib.QK_OK
+    assert lib.qk_cache_reserve(None, 64) == _lib.QK_ERR_INVALID_ARGUMENT
 
 
 def test_grouped_entry_points_reject_null_handles():

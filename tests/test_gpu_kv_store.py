@@ -87,12 +87,98 @@ def test_dimension_mismatch_and_range_errors(qk):
         c.value(7)
 
 
-def test_capacity_is_out_of_range(qk):
-    c = qk.KvCache(qk.CacheConfig(head_dim=2, page_size=2), capacity=2)
-    c.append([1, 2], [3, 4])
-    c.append([1, 2], [3, 4])
+def test_kv_cache_grows_past_its_capacity(qk, oracle_c):
+    """The reference's KvCache grows without bound (kv_store.cpp:24-29); the GPU KvCache starts
+    at `capacity` and doubles through qk_cache_reserve, keeping pages and metadata bitwise."""
+    rng = np.random.default_rng(3)
+    d, S = 5, 3
+    keys = half(rng.standard_normal((200, d)))
+    vals = half(rng.standard_normal((200, d)))
+    c = qk.KvCache(qk.CacheConfig(head_dim=d, page_size=S), capacity=2)
+    for t in range(70):  # 2 -> 4 -> ... -> 128
+        assert c.append(keys[t], vals[t]) == t
+    c.extend(keys[70:], vals[70:])  # one reserve for the bulk
+    assert c.token_count() == 200 and c.page_count() == 67
+    assert c.quest_cache.max_tokens >= 200
+    mn, mx = c.quest_cache.read_metadata(0, 0, 0)
+    omn, omx = oracle_c.metadata(keys, S)
+    assert np.array_equal(mn.astype(np.float32).view(np.uint32), omn.view(np.uint32))
+    assert np.array_equal(mx.astype(np.float32).view(np.uint32), omx.view(np.uint32))
+    k, v = c.quest_cache.read_kv(0, 0, 0, 0, 200)
+    assert np.array_equal(k, keys.astype(np.float16)) and np.array_equal(v, vals.astype(np.float16))
+
+
+def test_kv_cache_growth_stops_at_the_page_limit(qk):
+    c = qk.KvCache(qk.CacheConfig(head_dim=1, page_size=1), capacity=16)
+    c.extend(np.ones((16384, 1)), np.ones((16384, 1)))
+    assert c.token_count() == 16384
+    with pytest.raises(NotImplementedError):
+        c.append([1], [1])
+    assert c.token_count() == 16384
+
+
+def test_quest_cache_capacity_is_out_of_range(qk):
+    """The batched cache never grows implicitly: a full slice raises until reserve()."""
+    qc = qk.QuestCache(2, 2, max_tokens=2)
+    one = torch.ones((1, 1, 2), dtype=torch.float16, device="cuda")
+    qc.append(0, one, one)
+    qc.append(0, one, one)
     with pytest.raises(IndexError):
-        c.append([1, 2], [3, 4])
+        qc.append(0, one, one)
+    qc.reserve(3)
+    qc.append(0, one, one)
+    assert qc.token_count() == 3
+
+
+def test_reserve_keeps_every_slice_and_the_step_matches(qk, oracle_c):
+    """Multi-layer, batched, GQA cache grown mid-sequence: every (layer, sequence, KV head)
+    slice keeps its pages, metadata and length, and the fused step then equals the oracle."""
+    rng = np.random.default_rng(11)
+    Lyr, B, Hq, Hkv, d, S = 2, 2, 4, 2, 128, 16
+    lens = [700, 333]
+    qc = qk.QuestCache(d, S, num_layers=Lyr, max_batch=B, num_q_heads=Hq, num_kv_heads=Hkv,
+                       max_tokens=max(lens))
+    keys = [[half(rng.standard_normal((Hkv, L, d)) / np.sqrt(d)) for L in lens] for _ in range(Lyr)]
+    vals = [[half(rng.standard_normal((Hkv, L, d)) / np.sqrt(d)) for L in lens] for _ in range(Lyr)]
+    for layer in range(Lyr):
+        for b in range(B):
+            qc.prefill(layer, b, torch.from_numpy(keys[layer][b]).half().cuda(),
+                       torch.from_numpy(vals[layer][b]).half().cuda())
+    bytes_before = qc._lib.qk_cache_device_bytes(qc._h)
+    qc.reserve(5000)
+    assert qc.max_tokens == 5000 and qc.max_pages == 313
+    assert qc._lib.qk_cache_device_bytes(qc._h) > bytes_before
+    for layer in range(Lyr):
+        for b in range(B):
+            assert qc.token_count(layer, b) == lens[b]
+            for h in range(Hkv):
+                mn, mx = qc.read_metadata(layer, b, h)
+                omn, omx = oracle_c.metadata(keys[layer][b][h], S)
+                assert np.array_equal(mn.astype(np.float32).view(np.uint32), omn.view(np.uint32))
+                assert np.array_equal(mx.astype(np.float32).view(np.uint32), omx.view(np.uint32))
+    # Steps on layer 1 after the growth: append, estimate, select, attend against the oracle.
+    G = Hq // Hkv
+    for _ in range(2):
+        q = half(rng.standard_normal((B, Hq, d)) / np.sqrt(d))
+        kn = half(rng.standard_normal((B, Hkv, d)) / np.sqrt(d))
+        vn = half(rng.standard_normal((B, Hkv, d)) / np.sqrt(d))
+        for b in range(B):
+            keys[1][b] = np.concatenate([keys[1][b], kn[b][:, None]], axis=1)
+            vals[1][b] = np.concatenate([vals[1][b], vn[b][:, None]], axis=1)
+        P = qc.max_pages
+        pages = torch.full((B, Hq, P), -1, dtype=torch.int32, device="cuda")
+        counts = torch.zeros((B, Hq), dtype=torch.int32, device="cuda")
+        t = lambda a: torch.from_numpy(a).half().cuda()  # noqa: E731
+        out = qc.decode_step(1, t(q), t(kn), t(vn), 256, pages=pages, counts=counts)
+        qc.check_status()
+        out, pages, counts = out.cpu().numpy(), pages.cpu().numpy(), counts.cpu().numpy()
+        for b in range(B):
+            for h in range(Hq):
+                _, p_want, o_want = oracle_c.quest_step(q[b, h], keys[1][b][h // G],
+                                                        vals[1][b][h // G], S, 256)
+                assert pages[b, h, :counts[b, h]].tolist() == p_want.tolist()
+                err = np.linalg.norm(out[b, h] - o_want) / np.linalg.norm(o_want)
+                assert err <= 1e-5
 
 
 def test_metadata_equals_rescan_property(qk, oracle_c):
