@@ -1,16 +1,82 @@
 // microbench_launch.cu -- host-step launch costs: a 128-CTA, 4-CTA-cluster, 512-thread kernel
 // (the fused decode kernel's launch shape) that writes a host-mapped completion word, launched
 // (A) with cudaLaunchKernelEx (cluster + PDL attributes) or (B) as a captured 1-node CUDA
-// graph, the host spinning on the word after each launch.  Prints microseconds per call.
+// graph, the host spinning on the word after each launch; (C) a persistent kernel woken by a
+// host-written doorbell word (CTA 0 polls host memory and broadcasts through device memory;
+// C' every CTA polls the host word).  Every variant reads a 192-byte row of host-mapped input
+// per CTA, like the host step's zero-copy query reads.  Prints microseconds per call.
 #include <chrono>
+#include <cstdlib>
 #include <cstdio>
 #include <cuda_runtime.h>
 
-__global__ void __launch_bounds__(512, 1) k_done(volatile unsigned* flag, unsigned seq) {
+__device__ int g_sink;
+__device__ unsigned g_go, g_count;
+
+__device__ __forceinline__ void read_input(const int4* in) {
+    if (threadIdx.x < 12) {
+        const int4 v = in[blockIdx.x * 12 + threadIdx.x];
+        if (v.x == 0x12345) g_sink = v.y;
+    }
+}
+
+__global__ void __launch_bounds__(512, 1) k_done(volatile unsigned* flag, unsigned seq, const int4* in) {
+    read_input(in);
     __syncthreads();
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         __threadfence_system();
         *flag = seq;
+    }
+}
+
+__device__ __forceinline__ unsigned ld_acq_sys(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned ld_acq_gpu(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// mode 0: CTA 0 polls the host doorbell and broadcasts via g_go; mode 1: every CTA polls host.
+// Exits on doorbell 0xffffffff or after 1 s without a new command.
+__global__ void __launch_bounds__(512, 1) k_persist(const unsigned* bell, unsigned* flag, const int4* in,
+                                                   int mode) {
+    __shared__ unsigned s_cmd;
+    unsigned last = 0;
+    for (;;) {
+        if (threadIdx.x == 0) {
+            const unsigned long long t0 = gtimer();
+            unsigned v;
+            if (mode == 0 && blockIdx.x != 0) {
+                while ((v = ld_acq_gpu(&g_go)) == last && gtimer() - t0 < 1000000000ull) {}
+            } else {
+                while ((v = ld_acq_sys(bell)) == last && gtimer() - t0 < 1000000000ull) {}
+                if (mode == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&g_go), "r"(v == last ? 0xffffffffu : v) : "memory");
+            }
+            s_cmd = v == last ? 0xffffffffu : v;
+        }
+        __syncthreads();
+        const unsigned cmd = s_cmd;
+        if (cmd == 0xffffffffu) return;
+        last = cmd;
+        read_input(in);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            if (atomicAdd(&g_count, 1u) == gridDim.x - 1) {
+                g_count = 0;
+                __threadfence_system();
+                asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(cmd) : "memory");
+            }
+        }
     }
 }
 
@@ -20,6 +86,13 @@ int main() {
     unsigned* d;
     cudaHostGetDevicePointer((void**)&d, h, 0);
     *(volatile unsigned*)h = 0;
+    int4 *hin, *din;
+    cudaHostAlloc(&hin, 128 * 12 * 16, cudaHostAllocMapped);
+    cudaHostGetDevicePointer((void**)&din, hin, 0);
+    unsigned *hbell, *dbell;
+    cudaHostAlloc(&hbell, 64, cudaHostAllocMapped);
+    cudaHostGetDevicePointer((void**)&dbell, hbell, 0);
+    *(volatile unsigned*)hbell = 0;
     cudaStream_t st;
     cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
     cudaLaunchConfig_t cfg{};
@@ -36,16 +109,23 @@ int main() {
     cfg.attrs = at;
     cfg.numAttrs = 2;
     unsigned seq = 0;
-    auto spin = [&](unsigned s) { while (__atomic_load_n(h, __ATOMIC_ACQUIRE) != s) {} };
+    auto spin = [&](unsigned s) {
+        const auto ts = std::chrono::steady_clock::now();
+        while (__atomic_load_n(h, __ATOMIC_ACQUIRE) != s)
+            if (std::chrono::steady_clock::now() - ts > std::chrono::seconds(3)) {
+                printf("no completion for %u\n", s);
+                exit(1);
+            }
+    };
     const int N = 2000;
-    for (int i = 0; i < 100; ++i) { cudaLaunchKernelEx(&cfg, k_done, (volatile unsigned*)d, ++seq); spin(seq); }
+    for (int i = 0; i < 100; ++i) { cudaLaunchKernelEx(&cfg, k_done, (volatile unsigned*)d, ++seq, (const int4*)din); spin(seq); }
     auto t0 = std::chrono::steady_clock::now();
-    for (int i = 0; i < N; ++i) { cudaLaunchKernelEx(&cfg, k_done, (volatile unsigned*)d, ++seq); spin(seq); }
+    for (int i = 0; i < N; ++i) { cudaLaunchKernelEx(&cfg, k_done, (volatile unsigned*)d, ++seq, (const int4*)din); spin(seq); }
     auto t1 = std::chrono::steady_clock::now();
     printf("A cudaLaunchKernelEx (cluster 4 + PDL) + spin: %.2f us/call\n", std::chrono::duration<double, std::micro>(t1 - t0).count() / N);
     cfg.numAttrs = 1;  // no PDL
     t0 = std::chrono::steady_clock::now();
-    for (int i = 0; i < N; ++i) { cudaLaunchKernelEx(&cfg, k_done, (volatile unsigned*)d, ++seq); spin(seq); }
+    for (int i = 0; i < N; ++i) { cudaLaunchKernelEx(&cfg, k_done, (volatile unsigned*)d, ++seq, (const int4*)din); spin(seq); }
     t1 = std::chrono::steady_clock::now();
     printf("A' cudaLaunchKernelEx (cluster 4) + spin:      %.2f us/call\n", std::chrono::duration<double, std::micro>(t1 - t0).count() / N);
     // B: graph; the sequence number comes from device memory bumped by a second node? Use a
@@ -54,7 +134,7 @@ int main() {
     cudaGraphExec_t ge;
     cudaStreamBeginCapture(st, cudaStreamCaptureModeGlobal);
     cfg.numAttrs = 2;
-    cudaLaunchKernelEx(&cfg, k_done, (volatile unsigned*)d, 0u);
+    cudaLaunchKernelEx(&cfg, k_done, (volatile unsigned*)d, 0u, (const int4*)din);
     cudaStreamEndCapture(st, &g);
     cudaGraphInstantiate(&ge, g, 0);
     size_t n = 0;
@@ -67,7 +147,7 @@ int main() {
     volatile unsigned* dp = (volatile unsigned*)d;
     for (int i = 0; i < 100; ++i) {
         unsigned s = ++seq;
-        void* args[2] = {&dp, &s};
+        void* args[3] = {&dp, &s, &din};
         kp.kernelParams = args;
         cudaGraphExecKernelNodeSetParams(ge, node, &kp);
         cudaGraphLaunch(ge, st);
@@ -76,7 +156,7 @@ int main() {
     t0 = std::chrono::steady_clock::now();
     for (int i = 0; i < N; ++i) {
         unsigned s = ++seq;
-        void* args[2] = {&dp, &s};
+        void* args[3] = {&dp, &s, &din};
         kp.kernelParams = args;
         cudaGraphExecKernelNodeSetParams(ge, node, &kp);
         cudaGraphLaunch(ge, st);
@@ -84,6 +164,23 @@ int main() {
     }
     t1 = std::chrono::steady_clock::now();
     printf("B graph launch (+ param update) + spin:        %.2f us/call\n", std::chrono::duration<double, std::micro>(t1 - t0).count() / N);
+    for (int mode = 0; mode < 2; ++mode) {
+        cfg.numAttrs = 1;
+        *(volatile unsigned*)hbell = 0;
+        *(volatile unsigned*)h = 0;
+        cudaLaunchKernelEx(&cfg, k_persist, (const unsigned*)dbell, d, (const int4*)din, mode);
+        unsigned s = 0;
+        auto ring = [&](unsigned v) { __atomic_store_n(hbell, v, __ATOMIC_RELEASE); };
+        for (int i = 0; i < 100; ++i) { ring(++s); spin(s); }
+        t0 = std::chrono::steady_clock::now();
+        for (int i = 0; i < N; ++i) { ring(++s); spin(s); }
+        t1 = std::chrono::steady_clock::now();
+        ring(0xffffffffu);
+        cudaStreamSynchronize(st);
+        printf("C%s persistent, doorbell (%s) + spin:    %.2f us/call\n", mode ? "'" : " ",
+               mode ? "all CTAs poll host" : "CTA 0 polls, device broadcast",
+               std::chrono::duration<double, std::micro>(t1 - t0).count() / N);
+    }
     printf("(%s)\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
 }
