@@ -42,6 +42,7 @@
 #ifndef QUESTKV_B200_H
 #define QUESTKV_B200_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -239,13 +240,20 @@ QK_API int qk_decode_step(qk_cache *cache, uint32_t layer, const uint16_t *q, co
                    void *out, int32_t out_dtype, int32_t *pages_out, uint32_t pages_stride,
                    int32_t *counts_out, void *stream);
 
-/* Same step from HOST buffers (pinned or pageable), synchronous: q/k/v are copied into a
- * pinned, device-mapped staging buffer that the kernel reads directly, and the kernel
- * writes the fp32 output there (zero-copy); one launch and one synchronisation per call.
- * The reference-facing call for callers that keep activations on the host. */
+/* Same step from HOST buffers (pinned or pageable), synchronous, one launch and one
+ * synchronisation per call.  The kernel reads q/k/v and writes the fp32 output over PCIe
+ * (zero-copy): in place when a buffer is pinned and device-mapped (qk_host_alloc,
+ * cudaHostAlloc, cudaHostRegister), else through the cache's pinned staging buffer (a host
+ * memcpy each way).  The reference-facing call for callers that keep activations on the
+ * host. */
 QK_API int qk_decode_step_host(qk_cache *cache, uint32_t layer, const uint16_t *q_host,
                         const uint16_t *k_host, const uint16_t *v_host, uint32_t batch,
                         const qk_selection_cfg *cfg, float *out_host, void *stream);
+
+/* Pinned, device-mapped host memory for the host-buffer entry points' inputs and outputs
+ * (read and written by the kernels in place); nullptr on failure.  Free with qk_host_free. */
+QK_API void *qk_host_alloc(size_t bytes);
+QK_API void qk_host_free(void *ptr);
 
 /* Host-buffer forms of the entry points above, for callers that keep activations on the
  * host (the questkv:: C++ layer in questkv_b200.hpp binds these).  Each stages its

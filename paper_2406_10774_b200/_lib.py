@@ -64,6 +64,8 @@ SIGNATURES = {
     "qk_cache_device_bytes": (ctypes.c_uint64, [_P]),
     "qk_cache_max_pages": (ctypes.c_uint32, [_P]),
     "qk_cache_reserve": (ctypes.c_int, [_P, ctypes.c_uint32]),
+    "qk_host_alloc": (ctypes.c_void_p, [ctypes.c_size_t]),
+    "qk_host_free": (None, [ctypes.c_void_p]),
     "qk_token_count": (ctypes.c_int, [_P, _U32, _U32, ctypes.POINTER(_U32)]),
     "qk_page_count": (ctypes.c_int, [_P, _U32, _U32, ctypes.POINTER(_U32)]),
     "qk_reset": (ctypes.c_int, [_P, _U32, _P]),

@@ -98,6 +98,27 @@ int dmalloc(qk_cache* c, T** p, size_t count) {
     return cuda_check(cudaMemset(*p, 0, bytes ? bytes : 16), "cudaMemset");
 }
 
+// Pinned, mapped blocks handed out by qk_host_alloc: [host address, (bytes, device view)].
+// Caller buffers inside one of them are read and written by the host step's kernel in place;
+// a registry lookup costs ~50 ns where cudaPointerGetAttributes costs ~1 us per pointer.
+struct HostBlock {
+    size_t bytes;
+    unsigned char* dev;
+};
+std::mutex g_host_mu;
+std::map<uintptr_t, HostBlock> g_host_blocks;
+
+template <typename T>
+T* mapped_host(T* p, size_t bytes) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    std::lock_guard<std::mutex> lock(g_host_mu);
+    auto it = g_host_blocks.upper_bound(a);
+    if (it == g_host_blocks.begin()) return nullptr;
+    --it;
+    if (a + bytes > it->first + it->second.bytes) return nullptr;
+    return reinterpret_cast<T*>(it->second.dev + (a - it->first));
+}
+
 void free_cache(qk_cache* c) {
     void* ptrs[] = {c->k_pool,    c->v_pool,    c->meta,      c->d_len,     c->ws_partial,
                     c->ws_ticket, c->d_status,  c->ws_scores, c->ws_pages,  c->ws_counts,
@@ -865,14 +886,27 @@ int qk_decode_step_host(qk_cache* c, uint32_t layer, const uint16_t* q_host,
         c->done_flag_dev = reinterpret_cast<uint32_t*>(c->host_stage_dev + in_max + out_max);
         *reinterpret_cast<volatile uint32_t*>(c->host_stage + in_max + out_max) = 0;
     }
+    // Caller buffers that are already pinned and device-mapped (cudaHostAlloc, torch
+    // pin_memory, cudaHostRegister) are read and written by the kernel in place; pageable
+    // ones go through the staging buffer.
     uint16_t* hq = reinterpret_cast<uint16_t*>(c->host_stage);
-    std::memcpy(hq, q_host, nq * 2);
-    if (k_host) {
-        std::memcpy(hq + nq, k_host, nkv * 2);
-        std::memcpy(hq + nq + nkv, v_host, nkv * 2);
+    const uint16_t* dq = mapped_host(q_host, nq * 2);
+    const uint16_t* dk = k_host ? mapped_host(k_host, nkv * 2) : nullptr;
+    const uint16_t* dv = k_host ? mapped_host(v_host, nkv * 2) : nullptr;
+    if (!dq) {
+        std::memcpy(hq, q_host, nq * 2);
+        dq = reinterpret_cast<const uint16_t*>(c->host_stage_dev);
     }
-    const uint16_t* dq = reinterpret_cast<const uint16_t*>(c->host_stage_dev);
-    float* dout = reinterpret_cast<float*>(c->host_stage_dev + in_max);
+    if (k_host && !dk) {
+        std::memcpy(hq + nq, k_host, nkv * 2);
+        dk = reinterpret_cast<const uint16_t*>(c->host_stage_dev) + nq;
+    }
+    if (k_host && !dv) {
+        std::memcpy(hq + nq + nkv, v_host, nkv * 2);
+        dv = reinterpret_cast<const uint16_t*>(c->host_stage_dev) + nq + nkv;
+    }
+    float* mapped_out = mapped_host(out_host, size_t(batch) * c->Hq * hd * 4);
+    float* dout = mapped_out ? mapped_out : reinterpret_cast<float*>(c->host_stage_dev + in_max);
     // Completion: the fused kernel's last unit publishes `seq` in the mapped word, so the host
     // spins on it (~1 us after the last output lands) instead of synchronising the stream.
     // Paths that do not consume the request (unfused fallback) synchronise as before.
@@ -883,8 +917,8 @@ int qk_decode_step_host(qk_cache* c, uint32_t layer, const uint16_t* q_host,
     if (c->host_graphs.size() != c->L) c->host_graphs.resize(c->L);
     static const int no_graph = getenv("QK_NO_HOST_GRAPH") ? 1 : 0;  // read once
     c->host_graph_mode = !no_graph;
-    int rc = qk_decode_step(c, layer, dq, k_host ? dq + nq : nullptr, k_host ? dq + nq + nkv : nullptr,
-                            batch, cfg, dout, QK_DTYPE_F32, nullptr, 0, nullptr, stream);
+    int rc = qk_decode_step(c, layer, dq, dk, dv, batch, cfg, dout, QK_DTYPE_F32, nullptr, 0,
+                            nullptr, stream);
     c->host_graph_mode = false;
     const bool signalled = c->pending_done_flag == nullptr;  // consumed by a fused launch
     c->pending_done_flag = nullptr;
@@ -905,8 +939,33 @@ int qk_decode_step_host(qk_cache* c, uint32_t layer, const uint16_t* q_host,
     } else if (!rc) {
         rc = cuda_check(cudaStreamSynchronize(st), "qk_decode_step_host");
     }
-    if (!rc) std::memcpy(out_host, c->host_stage + in_max, size_t(batch) * c->Hq * hd * 4);
+    if (!rc && !mapped_out) std::memcpy(out_host, c->host_stage + in_max, size_t(batch) * c->Hq * hd * 4);
     return rc;
+}
+
+void* qk_host_alloc(size_t bytes) {
+    void* p = nullptr;
+    void* d = nullptr;
+    if (bytes == 0) bytes = 16;
+    if (cudaHostAlloc(&p, bytes, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess ||
+        cudaHostGetDevicePointer(&d, p, 0) != cudaSuccess) {
+        cudaGetLastError();
+        if (p) cudaFreeHost(p);
+        set_error(QK_ERR_CUDA, "qk_host_alloc: cudaHostAlloc failed");
+        return nullptr;
+    }
+    std::lock_guard<std::mutex> lock(g_host_mu);
+    g_host_blocks[reinterpret_cast<uintptr_t>(p)] = HostBlock{bytes, static_cast<unsigned char*>(d)};
+    return p;
+}
+
+void qk_host_free(void* p) {
+    if (!p) return;
+    {
+        std::lock_guard<std::mutex> lock(g_host_mu);
+        if (g_host_blocks.erase(reinterpret_cast<uintptr_t>(p)) == 0) return;  // not ours
+    }
+    cudaFreeHost(p);
 }
 
 // ---- host-buffer variants (the questkv:: C++ layer, include/questkv_b200.hpp) ----------

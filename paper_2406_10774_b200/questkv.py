@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import weakref
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
 
@@ -63,6 +64,21 @@ def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
 def _sel_cfg(token_budget: int, force_include_recent: bool, per_layer_enabled: bool):
     return qk_selection_cfg(int(token_budget), int(bool(force_include_recent)),
                             int(bool(per_layer_enabled)))
+
+
+def host_empty(shape, dtype) -> np.ndarray:
+    """A numpy array in pinned, device-mapped host memory (qk_host_alloc), freed when the last
+    view of it goes away.  decode_step_host reads and writes such arrays in place (no staging
+    copy); other host arrays work too, through the cache's staging buffer."""
+    dtype = np.dtype(dtype)
+    nbytes = int(np.prod(shape)) * dtype.itemsize
+    lib = _lib.load()
+    p = lib.qk_host_alloc(max(nbytes, 1))
+    if not p:
+        check(_lib.QK_ERR_CUDA)
+    block = (ctypes.c_uint8 * max(nbytes, 1)).from_address(p)
+    weakref.finalize(block, lib.qk_host_free, p)
+    return np.frombuffer(block, dtype=dtype, count=int(np.prod(shape))).reshape(shape)
 
 
 class QuestCache:

@@ -280,3 +280,53 @@ def test_decode_step_host_consecutive_steps(qk):
         out_d = b_.decode_step(0, torch.from_numpy(q).cuda(), torch.from_numpy(kn).cuda(),
                                torch.from_numpy(vn).cuda(), 512)
         assert np.array_equal(out_h, out_d.cpu().numpy()), step
+
+
+@pytest.mark.parametrize("pin", ["all", "q_out", "kv"])
+def test_decode_step_host_pinned_buffers_in_place(qk, pin):
+    """Caller buffers from qk_host_alloc (questkv.host_empty) are read and written by the
+    kernel in place; any mix with pageable or torch-pinned (staged) buffers, and a new
+    buffer set every step (the host step's graph re-keys), gives the device step's output
+    bitwise."""
+    rng = np.random.default_rng(21)
+    B, Hq, Hkv, d, S = 2, 8, 2, 128, 16
+    a, _, _ = _layer(qk, np.random.default_rng(22), B, Hq, Hkv, d, S, [2500, 77])
+    b_, _, _ = _layer(qk, np.random.default_rng(22), B, Hq, Hkv, d, S, [2500, 77])
+
+    def buf(a_np, pinned):
+        if not pinned:  # alternate pageable and torch-pinned (both staged)
+            return torch.from_numpy(a_np.copy()).pin_memory().numpy() if step % 2 else a_np.copy()
+        h = qk.host_empty(a_np.shape, a_np.dtype)
+        h[...] = a_np
+        return h
+
+    for step in range(4):
+        q = half(rng.standard_normal((B, Hq, d)) / np.sqrt(d)).astype(np.float16)
+        kn = half(rng.standard_normal((B, Hkv, d)) / np.sqrt(d)).astype(np.float16)
+        vn = half(rng.standard_normal((B, Hkv, d)) / np.sqrt(d)).astype(np.float16)
+        out = buf(np.zeros((B, Hq, d), np.float32), pin in ("all", "q_out"))
+        qh = buf(q, pin in ("all", "q_out"))
+        kh, vh = buf(kn, pin in ("all", "kv")), buf(vn, pin in ("all", "kv"))
+        got = a.decode_step_host(0, qh, kh, vh, 512, out=out)
+        want = b_.decode_step(0, torch.from_numpy(q).cuda(), torch.from_numpy(kn).cuda(),
+                              torch.from_numpy(vn).cuda(), 512)
+        assert got is out
+        assert np.array_equal(got, want.cpu().numpy()), step
+
+
+def test_host_alloc_is_pinned_and_mapped(qk):
+    import ctypes
+
+    from paper_2406_10774_b200 import _lib
+
+    lib = _lib.load()
+    p = lib.qk_host_alloc(4096)
+    assert p
+    arr = (ctypes.c_uint8 * 4096).from_address(p)
+    arr[0], arr[4095] = 7, 9
+    assert arr[0] == 7 and arr[4095] == 9
+    lib.qk_host_free(p)
+    lib.qk_host_free(None)
+    h = qk.host_empty((3, 5), np.float32)
+    h[...] = 2.5
+    assert h.shape == (3, 5) and float(h.sum()) == 37.5
