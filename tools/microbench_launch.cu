@@ -29,6 +29,28 @@ __global__ void __launch_bounds__(512, 1) k_done(volatile unsigned* flag, unsign
     }
 }
 
+// D: the inputs travel in the launch's parameter block (24 KB = q, k, v of a cfg2 layer)
+// instead of being read from host memory by the kernel.
+struct Blob {
+    int4 data[1536];
+};
+__global__ void __launch_bounds__(512, 1) k_blob(volatile unsigned* flag, unsigned seq,
+                                                 const __grid_constant__ Blob blob) {
+    if (threadIdx.x < 12) {
+        const int4 v = blob.data[blockIdx.x * 12 + threadIdx.x];
+        if (v.x == 0x12345) g_sink = v.y;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(&g_count, 1u) == gridDim.x - 1) {
+            g_count = 0;
+            __threadfence_system();
+            *flag = seq;
+        }
+    }
+}
+
 __device__ __forceinline__ unsigned ld_acq_sys(const unsigned* p) {
     unsigned v;
     asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -164,6 +186,50 @@ int main() {
     }
     t1 = std::chrono::steady_clock::now();
     printf("B graph launch (+ param update) + spin:        %.2f us/call\n", std::chrono::duration<double, std::micro>(t1 - t0).count() / N);
+    {
+        static Blob blob;
+        cfg.numAttrs = 1;
+        for (int i = 0; i < 100; ++i) {
+            blob.data[0].x = i;
+            cudaLaunchKernelEx(&cfg, k_blob, (volatile unsigned*)d, ++seq, blob);
+            spin(seq);
+        }
+        t0 = std::chrono::steady_clock::now();
+        for (int i = 0; i < N; ++i) {
+            blob.data[0].x = i;
+            cudaLaunchKernelEx(&cfg, k_blob, (volatile unsigned*)d, ++seq, blob);
+            spin(seq);
+        }
+        t1 = std::chrono::steady_clock::now();
+        printf("D cudaLaunchKernelEx, 24 KB inputs as params:  %.2f us/call\n",
+               std::chrono::duration<double, std::micro>(t1 - t0).count() / N);
+        // D': the same through a 1-node graph whose parameters are updated per call.
+        cudaGraph_t gb;
+        cudaGraphExec_t geb;
+        cudaStreamBeginCapture(st, cudaStreamCaptureModeGlobal);
+        cudaLaunchKernelEx(&cfg, k_blob, (volatile unsigned*)d, 0u, blob);
+        cudaStreamEndCapture(st, &gb);
+        cudaGraphInstantiate(&geb, gb, 0);
+        cudaGraphNode_t nb;
+        size_t nn = 1;
+        cudaGraphGetNodes(gb, &nb, &nn);
+        cudaKernelNodeParams kpb;
+        cudaGraphKernelNodeGetParams(nb, &kpb);
+        volatile unsigned* dpp = (volatile unsigned*)d;
+        auto launch_blob = [&](unsigned sq) {
+            void* args[3] = {&dpp, &sq, &blob};
+            kpb.kernelParams = args;
+            cudaGraphExecKernelNodeSetParams(geb, nb, &kpb);
+            cudaGraphLaunch(geb, st);
+            spin(sq);
+        };
+        for (int i = 0; i < 100; ++i) { blob.data[0].x = i; launch_blob(++seq); }
+        t0 = std::chrono::steady_clock::now();
+        for (int i = 0; i < N; ++i) { blob.data[0].x = i; launch_blob(++seq); }
+        t1 = std::chrono::steady_clock::now();
+        printf("D' graph + param update, 24 KB params:        %.2f us/call\n",
+               std::chrono::duration<double, std::micro>(t1 - t0).count() / N);
+    }
     for (int mode = 0; mode < 2; ++mode) {
         cfg.numAttrs = 1;
         *(volatile unsigned*)hbell = 0;
