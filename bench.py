@@ -446,13 +446,19 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # One event after every step too: the per-step distribution (median, p10,
+    # p90); the headline is the first-to-last span.
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     with ClockSampler(local) as clocks:
         with torch.cuda.stream(stream):
             ev0.record(stream)
-            for i in range(args.warmup, total_steps):
+            for j, i in enumerate(range(args.warmup, total_steps)):
                 step(i)
+                evs[j].record(stream)
             ev1.record(stream)
         stream.synchronize()
+    step_us = [ev0.elapsed_time(evs[0]) * 1e3 / NL] + [
+        evs[j - 1].elapsed_time(evs[j]) * 1e3 / NL for j in range(1, args.steps)]
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -644,6 +650,7 @@ def run_ours(args):
             "bytes_model": bytes_model,
             "peak_source": peak_src,
         },
+        "step_distribution_us_per_layer": percentiles(step_us),
         "kernel_breakdown_us": breakdown,
         "gpu_launches": int(kernels_per_step * args.steps),
         "clocks": clocks.summary(),
@@ -655,6 +662,13 @@ def run_ours(args):
     print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
+
+
+def percentiles(xs):
+    """p10 / median / p90 of per-step µs per layer (nearest rank)."""
+    ys = sorted(xs)
+    pick = lambda f: round(ys[min(len(ys) - 1, int(f * (len(ys) - 1) + 0.5))], 3)  # noqa: E731
+    return {"p10": pick(0.1), "median": pick(0.5), "p90": pick(0.9), "n": len(ys)}
 
 
 def native_e2e(ctx, budget):
