@@ -801,8 +801,9 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
             // MHA selection the other warps prefetch into L2 the K/V pages the first radix
             // pass proves selected (pages i % C == rank: the cluster requests each once),
             // so HBM streams attention bytes while the boundary is still being resolved.
-            auto group_select = [&](auto nts_tag) {
+            auto group_select = [&](auto nts_tag, auto kpt_tag) {
                 constexpr int NTS = decltype(nts_tag)::value;
+                constexpr int KP = decltype(kpt_tag)::value;
                 constexpr int NGRP = kThreads / NTS;
                 auto* gsc = reinterpret_cast<SelectScratch<NTS>*>(smem);  // region A
                 const int grpi = tid / NTS, gt = tid % NTS;
@@ -843,17 +844,17 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
                 }
                 for (int g = grpi; g < G; g += NGRP) {
                     const unsigned long long* kg = keys + size_t(g) * p.key_cap;
-                    unsigned long long k16[kSelKpt];
-                    const ulonglong2* src = reinterpret_cast<const ulonglong2*>(kg + key_slot(uint32_t(gt) * kSelKpt));
-                    const bool has = uint32_t(gt) * kSelKpt < n_cand;  // rows past the keys stay out
+                    unsigned long long k16[KP];
+                    const ulonglong2* src = reinterpret_cast<const ulonglong2*>(kg + key_slot(uint32_t(gt) * KP));
+                    const bool has = uint32_t(gt) * KP < n_cand;  // rows past the keys stay out
 #pragma unroll
-                    for (int j = 0; j < kSelKpt / 2; ++j) {
+                    for (int j = 0; j < KP / 2; ++j) {
                         const ulonglong2 v = has ? src[j] : make_ulonglong2(0ull, 0ull);
                         k16[2 * j] = v.x;
                         k16[2 * j + 1] = v.y;
                     }
                     if (g == 0) stamp(p.probe, 10);
-                    block_select_reg<NTS, kSelKpt>(k16, n_cand, target, kg[0], sel + g * kMaxFusedK,
+                    block_select_reg<NTS, KP>(k16, n_cand, target, kg[0], sel + g * kMaxFusedK,
                                                    gsc[grpi], gt, 1 + grpi,
                                                    g == 0 ? p.probe : nullptr, G == 1 ? 7 : -1,
                                                    kThreads);
@@ -861,10 +862,17 @@ __global__ void __launch_bounds__(kThreads, 1) decode_fused_kernel(const FusedPa
 
                 }
             };
-            if (smem_keys && n_cand <= uint32_t(kSelThreads * kSelKpt)) {
-                group_select(std::integral_constant<int, kSelThreads>{});
+            if (G == 1 && smem_keys && n_cand <= uint32_t(kSelThreads * kSelKpt)) {
+                // MHA up to 2048 candidates: 256 threads x 8 keys (half the serial per-thread
+                // work of 128 x 16; 8 warps still prefetch): 19.19 -> 19.08 and 19.31 -> 19.21
+                // us/layer in two same-box A/Bs (tools/ab_bench.sh); 512 x 4 without the
+                // prefetch warps 19.24, with per-thread prefetch of its own proven keys 19.36.
+                group_select(std::integral_constant<int, 2 * kSelThreads>{},
+                             std::integral_constant<int, kSelKpt / 2>{});
+            } else if (smem_keys && n_cand <= uint32_t(kSelThreads * kSelKpt)) {
+                group_select(std::integral_constant<int, kSelThreads>{}, std::integral_constant<int, kSelKpt>{});
             } else if (smem_keys && n_cand <= uint32_t(2 * kSelThreads * kSelKpt)) {
-                group_select(std::integral_constant<int, 2 * kSelThreads>{});
+                group_select(std::integral_constant<int, 2 * kSelThreads>{}, std::integral_constant<int, kSelKpt>{});
             } else if (smem_keys && n_cand <= uint32_t(kThreads * kSelKpt)) {
                 for (int g = 0; g < G; ++g) {
                     const unsigned long long* kg = keys + size_t(g) * p.key_cap;
