@@ -127,6 +127,14 @@ __global__ void touch_pages(const char* __restrict__ p, size_t n, int* sink) {
     if (acc == 0x12345678) sink[0] = acc;
 }
 
+__global__ void fill_random(unsigned int* p, size_t n) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+        unsigned int x = unsigned(i) * 2654435761u ^ unsigned(i >> 32) * 40503u;
+        x ^= x >> 13; x *= 0x5bd1e995u; x ^= x >> 15;
+        p[i] = x & 0x3bff3bffu;  // two finite fp16 values
+    }
+}
+
 __global__ void flush(const int4* p, size_t n, int* sink) {
     int acc = 0;
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
@@ -141,7 +149,12 @@ int main() {
     int4* junk;
     const size_t junk_n = (size_t(getenv("BIGFLUSH") ? 4096 : 192) << 20) / 16;  // BIGFLUSH: TLB thrash
     cudaMalloc(&meta, meta_elems * 2);
-    cudaMemset(meta, 1, meta_elems * 2);
+    if (getenv("RANDOM_META")) {  // random fp16 bit patterns (constant data may be compressed)
+        fill_random<<<592, 512>>>(reinterpret_cast<unsigned int*>(meta), meta_elems / 2);
+        cudaDeviceSynchronize();
+    } else {
+        cudaMemset(meta, 1, meta_elems * 2);
+    }
     cudaMalloc(&sink, 4096);
     cudaMalloc(&junk, junk_n * 16);
     cudaMemset(junk, 0, junk_n * 16);
