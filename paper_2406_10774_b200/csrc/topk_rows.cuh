@@ -19,7 +19,7 @@ namespace qk {
 constexpr int kRowKpt = 16;
 constexpr uint32_t kRowMaxPages = 512u * kRowKpt;
 
-template <int NT, int G>
+template <int NT, int G, int KPT = kRowKpt>
 __global__ void __launch_bounds__(NT)
 topk_rows_kernel(const double* __restrict__ scores, uint32_t sstride,
                  const int32_t* __restrict__ len, uint32_t layer, uint32_t B,
@@ -37,7 +37,7 @@ topk_rows_kernel(const double* __restrict__ scores, uint32_t sstride,
         if (threadIdx.x == 0) counts[row] = int32_t(P);
         return;
     }
-    if (P > sstride || k_budget > pstride || P > uint32_t(NT) * kRowKpt) return;  // host-checked
+    if (P > sstride || k_budget > pstride || P > uint32_t(NT) * KPT) return;  // host-checked
     const uint32_t n_cand = force ? P - 1 : P;  // pages competing on score
     const uint32_t target = force ? k_budget - 1 : k_budget;
     const double* src = scores + size_t(row) * G * sstride;
@@ -53,23 +53,23 @@ topk_rows_kernel(const double* __restrict__ scores, uint32_t sstride,
     };
     if (target > 0) {
         const int t = threadIdx.x;
-        const uint32_t i0 = uint32_t(t) * kRowKpt;
-        unsigned long long key[kRowKpt];
-        if (G == 1 && i0 + kRowKpt <= n_cand && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+        const uint32_t i0 = uint32_t(t) * KPT;
+        unsigned long long key[KPT];
+        if (G == 1 && i0 + KPT <= n_cand && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
             // a full, aligned run: 16-byte loads
             const double2* s2 = reinterpret_cast<const double2*>(src + i0);
 #pragma unroll
-            for (int j = 0; j < kRowKpt / 2; ++j) {
+            for (int j = 0; j < KPT / 2; ++j) {
                 const double2 v = __ldcg(s2 + j);
                 key[2 * j] = order_key(__dadd_rn(v.x, 0.0));
                 key[2 * j + 1] = order_key(__dadd_rn(v.y, 0.0));
             }
         } else {
 #pragma unroll
-            for (int j = 0; j < kRowKpt; ++j) key[j] = i0 + j < n_cand ? score(i0 + j) : 0ull;
+            for (int j = 0; j < KPT; ++j) key[j] = i0 + j < n_cand ? score(i0 + j) : 0ull;
         }
         const unsigned long long ref = score(0);
-        block_select_reg<NT, kRowKpt>(key, n_cand, target, ref, out, sc, t, 1);
+        block_select_reg<NT, KPT>(key, n_cand, target, ref, out, sc, t, 1);
     }
     if (threadIdx.x == 0) {
         if (force) out[target] = int32_t(P - 1);
@@ -85,14 +85,21 @@ inline cudaError_t launch_topk_rows(uint32_t rows, uint32_t capacity, const doub
                                     uint32_t B, uint32_t rows_per_seq, uint32_t S,
                                     uint32_t k_budget, int force, int reduce, int32_t* pages,
                                     uint32_t pstride, int32_t* counts, cudaStream_t st) {
-#define QK_TOPK_ROWS(NT)                                                                        \
-    topk_rows_kernel<NT, G><<<rows, NT, 0, st>>>(scores, sstride, len, layer, B, rows_per_seq, \
-                                                 S, k_budget, force, reduce, pages, pstride,   \
-                                                 counts)
-    if (capacity <= 128u * kRowKpt) QK_TOPK_ROWS(128);
+#define QK_TOPK_ROWS_K(NT, KPT)                                                                  \
+    topk_rows_kernel<NT, G, KPT><<<rows, NT, 0, st>>>(scores, sstride, len, layer, B,            \
+                                                      rows_per_seq, S, k_budget, force, reduce,  \
+                                                      pages, pstride, counts)
+#define QK_TOPK_ROWS(NT) QK_TOPK_ROWS_K(NT, kRowKpt)
+    // A launch of at most one row per SM: twice the threads with half the keys each (the
+    // per-thread serial work of the radix pass halves; occupancy does not matter).
+    if (rows <= 148u && capacity > 128u * 8u && capacity <= 512u * 8u) {
+        if (capacity <= 256u * 8u) QK_TOPK_ROWS_K(256, 8);
+        else QK_TOPK_ROWS_K(512, 8);
+    } else if (capacity <= 128u * kRowKpt) QK_TOPK_ROWS(128);
     else if (capacity <= 256u * kRowKpt) QK_TOPK_ROWS(256);
     else QK_TOPK_ROWS(512);
 #undef QK_TOPK_ROWS
+#undef QK_TOPK_ROWS_K
     return cudaGetLastError();
 }
 
