@@ -21,6 +21,8 @@
 // loads of groups g+1.. .  MHA (G=1): each thread owns two adjacent pages (half2 reads,
 // two independent chains).  GQA (G>1): each thread owns one page and G chains, the
 // metadata is read once per KV head for all G query heads.
+#include <cstdlib>
+
 #include "qk_internal.cuh"
 
 namespace qk {
@@ -292,6 +294,120 @@ estimate_gqa_kernel(const __half* __restrict__ meta, const int32_t* __restrict__
     }
 }
 
+// Staged variant (PB = 8): the metadata pieces go through a kStages-deep cp.async pipeline
+// in shared memory instead of register double buffers, so a thread keeps ~kStages x 128 B in
+// flight without holding them in registers (more bytes in flight per SM, more CTAs per SM).
+// Each thread copies and later reads only its own pieces: no CTA barrier in the loop.
+constexpr int kStages = 4;
+
+template <int D, int G>
+__global__ void __launch_bounds__(kThreads)
+estimate_gqa_staged_kernel(const __half* __restrict__ meta, const int32_t* __restrict__ len,
+                           const __half* __restrict__ q, double* __restrict__ scores,
+                           uint32_t layer, uint32_t B, uint32_t Hkv, uint32_t S,
+                           uint32_t head_dim, size_t slice_meta, uint32_t mrow,
+                           uint32_t sstride) {
+    using GM = GqaGeom<G>;
+    constexpr int PB = GM::PB, PPC = GM::PPC, U = GM::UNROLL;
+    static_assert(PB == 8, "16-byte pieces");
+    extern __shared__ __align__(16) int4 stage[];  // [kStages][2][U][kThreads]
+    __shared__ double dw[G * D];
+    __shared__ unsigned char need[D];
+
+    const uint32_t bh = blockIdx.y;
+    const uint32_t b = bh / Hkv, kvh = bh % Hkv;
+    const uint32_t n_tok = static_cast<uint32_t>(len[layer * B + b]);
+    const uint32_t P = (n_tok + S - 1) / S;
+    const uint32_t page0 = blockIdx.x * PPC;
+    if (page0 >= P) return;
+    const int tid = threadIdx.x;
+    for (int i = tid; i < G * D; i += kThreads) {
+        const int g = i / D, c = i % D;
+        const double x = c < int(head_dim)
+                             ? double(__half2float(q[(size_t(b) * Hkv * G + size_t(kvh) * G + g) * head_dim + c]))
+                             : 0.0;
+        dw[i] = (x < 0.0) ? x : x * 0x1p1008;
+    }
+    __syncthreads();
+    for (int c = tid; c < D; c += kThreads) {
+        unsigned char m = 0;
+#pragma unroll
+        for (int g = 0; g < G; ++g) m |= (dw[g * D + c] < 0.0) ? 2 : 1;
+        need[c] = m;
+    }
+    __syncthreads();
+
+    const uint32_t pbase = page0 + uint32_t(tid) * PB;
+    if (pbase >= P) return;
+    const size_t s = (size_t(layer) * B + b) * Hkv + kvh;
+    const __half* mslice = meta + s * slice_meta;  // [2][D][mrow]
+    double acc[G][PB];
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+#pragma unroll
+        for (int j = 0; j < PB; ++j) acc[g][j] = 0.0;
+
+    constexpr int NB = D / U;  // channel blocks
+    auto slot = [&](int st, int row, int u) -> int4* {
+        return stage + ((st * 2 + row) * U + u) * kThreads + tid;
+    };
+    auto issue = [&](int cb) {
+        if (cb < NB) {
+            const int st = cb % kStages;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int c = cb * U + u;
+                const unsigned char m = need[c];
+                if (m & 2) cp_async16(slot(st, 0, u), mslice + size_t(c) * mrow + pbase);
+                if (m & 1) cp_async16(slot(st, 1, u), mslice + size_t(D + c) * mrow + pbase);
+            }
+        }
+        cp_async_commit();  // (empty groups keep the wait count uniform)
+    };
+#pragma unroll
+    for (int cb = 0; cb < kStages - 1; ++cb) issue(cb);
+#pragma unroll 1
+    for (int cb = 0; cb < NB; ++cb) {
+        cp_async_wait<kStages - 2>();
+        const int st = cb % kStages;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int c = cb * U + u;
+            const unsigned char m = need[c];
+            const int4 lo = (m & 2) ? *slot(st, 0, u) : make_int4(0, 0, 0, 0);
+            const int4 hi = (m & 1) ? *slot(st, 1, u) : make_int4(0, 0, 0, 0);
+            const unsigned short* l16 = reinterpret_cast<const unsigned short*>(&lo);
+            const unsigned short* h16 = reinterpret_cast<const unsigned short*>(&hi);
+            double xl[PB], xh[PB];
+#pragma unroll
+            for (int j = 0; j < PB; ++j) {
+                xl[j] = h2d(__ushort_as_half(l16[j]));
+                xh[j] = h2d_scaled(h16[j]);
+            }
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const double w = dw[g * D + c];
+                if (w < 0.0) {
+#pragma unroll
+                    for (int j = 0; j < PB; ++j) acc[g][j] = __fma_rn(w, xl[j], acc[g][j]);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < PB; ++j) acc[g][j] = __fma_rn(w, xh[j], acc[g][j]);
+                }
+            }
+        }
+        issue(cb + kStages - 1);  // into the slot read in the previous iteration
+    }
+#pragma unroll
+    for (int j = 0; j < PB; ++j) {
+        const uint32_t p = pbase + j;
+        if (p >= P || p >= sstride) break;
+#pragma unroll
+        for (int g = 0; g < G; ++g)
+            scores[(size_t(b) * Hkv * G + size_t(kvh) * G + g) * sstride + p] = acc[g][j];
+    }
+}
+
 template <int D, int G>
 int run(const qk_cache* c, uint32_t layer, const __half* q, uint32_t batch, double* scores,
         uint32_t stride, uint32_t max_pages, cudaStream_t st) {
@@ -303,6 +419,23 @@ int run(const qk_cache* c, uint32_t layer, const __half* q, uint32_t batch, doub
     } else {
         using GM = GqaGeom<G>;
         const dim3 grid((max_pages + GM::PPC - 1) / GM::PPC, batch * c->Hkv);
+        // G = 2, 4 (16-byte pieces): the cp.async-staged kernel (cfg4: 388 -> 374 us per
+        // layer step, 2-round A/B; deeper or narrower pipelines and 4 CTAs per SM were slower).
+        static const bool staged = getenv("QK_GQA_REGISTER_ESTIMATE") == nullptr;  // A/B switch
+        if constexpr (GM::PB == 8) {
+            if (staged) {
+                const size_t smem = size_t(kStages) * 2 * GM::UNROLL * kThreads * 16;
+                auto kern = estimate_gqa_staged_kernel<D, G>;
+                if (int rc = ensure_func_attrs(reinterpret_cast<const void*>(kern), smem,
+                                               c->desc.device, false, "estimate_gqa_staged"))
+                    return rc;
+                kern<<<grid, kThreads, smem, st>>>(c->meta, c->d_len, q, scores, layer, c->B,
+                                                   c->Hkv, c->S, c->desc.head_dim, c->slice_meta,
+                                                   c->Mrow, stride);
+                const_cast<qk_cache*>(c)->launches++;
+                return cuda_check(cudaGetLastError(), "estimate_kernel");
+            }
+        }
         estimate_gqa_kernel<D, G><<<grid, kThreads, 0, st>>>(
             c->meta, c->d_len, q, scores, layer, c->B, c->Hkv, c->S, c->desc.head_dim,
             c->slice_meta, c->Mrow, stride);
