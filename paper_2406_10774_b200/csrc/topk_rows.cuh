@@ -19,8 +19,10 @@ namespace qk {
 constexpr int kRowKpt = 16;
 constexpr uint32_t kRowMaxPages = 512u * kRowKpt;
 
+// The 512 x 16 form serves only wide launches (more rows than SMs): two CTAs per SM at 64
+// registers (some spills) beat one at 125 (cfg4: -4 us per layer step).
 template <int NT, int G, int KPT = kRowKpt>
-__global__ void __launch_bounds__(NT)
+__global__ void __launch_bounds__(NT, (NT >= 512 && KPT >= 16) ? 2 : 1)
 topk_rows_kernel(const double* __restrict__ scores, uint32_t sstride,
                  const int32_t* __restrict__ len, uint32_t layer, uint32_t B,
                  uint32_t rows_per_seq, uint32_t S, uint32_t k_budget, int force, int reduce,
