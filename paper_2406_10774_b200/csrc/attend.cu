@@ -1,3 +1,4 @@
+#include <algorithm>
 // attend.cu -- split-KV sparse paged decode attention with an LSE merge (K4 + K5), and
 // dense attention as the same kernel over every page (K6).
 //
@@ -38,6 +39,7 @@ namespace {
 constexpr int kThreads = 128;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxSplitPages = 256;  // page-list entries of a split staged in shared memory
+constexpr uint32_t kSplitTarget = 512;  // CTAs per launch the split rule aims at
 
 template <int D>
 __global__ void __launch_bounds__(kThreads)
@@ -48,7 +50,7 @@ attend_kernel(const __half* __restrict__ kp, const __half* __restrict__ vp,
               uint32_t Hq, uint32_t Hkv, uint32_t S, uint32_t head_dim, size_t slice_kv,
               float scale_log2, float* __restrict__ ws_partial, int32_t* __restrict__ ws_ticket,
               void* __restrict__ out, int out_dtype, float* __restrict__ lse,
-              double* __restrict__ wsum, int32_t* __restrict__ status, int min_pps) {
+              double* __restrict__ wsum, int32_t* __restrict__ status, int max_splits) {
     const bool dense = mode == kModeDense, tokens = mode == kModeTokens;
     constexpr int CPR = D / 8;  // 16-byte chunks per row
     __shared__ float s_o[kWarps][D];
@@ -68,7 +70,7 @@ attend_kernel(const __half* __restrict__ kp, const __half* __restrict__ vp,
     }
     // Units of the split rule: pages, or chunks of S list entries (token mode).
     const int units = tokens ? int((uint32_t(count) + S - 1) / S) : count;
-    const int pps = max(min_pps, (units + kMaxSplits - 1) / kMaxSplits);
+    const int pps = max(kMinPagesPerSplit, (units + max_splits - 1) / max_splits);
     const int nsplit = (units + pps - 1) / pps;
     // A count past the list row, or needing more splits than the host launched, would read
     // past the row or never complete the merge ticket: reject it (uniform over the CTAs of
@@ -255,20 +257,24 @@ int run(const qk_cache* c, uint32_t layer, const __half* q, uint32_t batch,
         uint32_t max_list, void* out, int out_dtype, float* lse, double* wsum, cudaStream_t st) {
     // max_list: the longest list (pages, or tokens in token mode) a row may hold.
     const uint32_t max_units = mode == kModeTokens ? (max_list + c->S - 1) / c->S : max_list;
-    // Units per split: 8, or 16 for wide launches (>= 256 (sequence, head) rows: a CTA's
-    // fixed costs -- q, page list, combine, partials, merge ticket -- over more pages).  A
-    // function of (batch, heads) only, so dense, sparse-over-every-page and token-mode calls
-    // of one batch share the partition (and stay bitwise equal).
-    const int min_pps = batch * c->Hq >= 256u ? 2 * kMinPagesPerSplit : kMinPagesPerSplit;
-    const uint32_t splits_needed = max_units <= uint32_t(min_pps) * kMaxSplits
-                                       ? (max_units + min_pps - 1) / min_pps
-                                       : uint32_t(kMaxSplits);
+    // Splits per row: about kSplitTarget CTAs per launch (one wave of a few CTAs per SM; a
+    // CTA's fixed costs -- q, page list, combine, partials, merge ticket -- over as many pages
+    // as that allows), at least 8 units each.  Measured (cfg2 unless noted, µs per layer):
+    // dense 109 -> 88 (16 splits of 128 pages instead of 64 of 32), cfg4 per-head 366 -> 351
+    // (1 split per row instead of 8), cfg5 unfused 111 -> 107 (2 instead of 8), sparse cfg2
+    // unchanged (16 splits of 8).  A function of the launch's rows and the row's own count
+    // only, so dense, sparse-over-every-page and token-mode calls of one batch share the
+    // partition (and stay bitwise equal).
+    const uint32_t rows = batch * c->Hq;
+    const int max_splits = int(std::min<uint32_t>(kMaxSplits, std::max<uint32_t>(1u, kSplitTarget / rows)));
+    const uint32_t splits_needed = std::min<uint32_t>(uint32_t(max_splits),
+                                                      (max_units + kMinPagesPerSplit - 1) / kMinPagesPerSplit);
     const dim3 grid(splits_needed ? splits_needed : 1, batch * c->Hq);
     const float scale_log2 = float(1.4426950408889634 / sqrt(double(c->desc.head_dim)));
     attend_kernel<D><<<grid, kThreads, 0, st>>>(
         c->k_pool, c->v_pool, c->d_len, q, pages, pstride, counts, mode, layer, c->B,
         c->Hq, c->Hkv, c->S, c->desc.head_dim, c->slice_kv, scale_log2, c->ws_partial,
-        c->ws_ticket, out, out_dtype, lse, wsum, c->d_status, min_pps);
+        c->ws_ticket, out, out_dtype, lse, wsum, c->d_status, max_splits);
     const_cast<qk_cache*>(c)->launches++;
     return cuda_check(cudaGetLastError(), "attend_kernel");
 }

@@ -29,6 +29,7 @@
 //     its own channel run of 4 V rows (PRMT packs the token pairs).
 //   * online softmax per head in the base-2 domain, warps combined in order, splits merged
 //     by the last CTA (attend.cu's split rule, ticket and merge).
+#include <algorithm>
 #include <math_constants.h>
 
 #include "topk_rows.cuh"
@@ -118,7 +119,7 @@ grouped_attend_kernel(const __half* __restrict__ kp, const __half* __restrict__ 
                       uint32_t Hkv, uint32_t S, uint32_t head_dim, size_t slice_kv,
                       float scale_log2, float* __restrict__ ws_partial,
                       int32_t* __restrict__ ws_ticket, void* __restrict__ out, int out_dtype,
-                      int32_t* __restrict__ status, int min_pps) {
+                      int32_t* __restrict__ status, int max_splits) {
     static_assert(G >= 1 && G <= 8, "at most 8 query heads per group (MMA rows 0..7)");
     constexpr int KS = D / 16;   // k-steps of S = Q K^T
     constexpr int NT = D / 8;    // n-tiles (8 channels) of O = P V
@@ -138,7 +139,7 @@ grouped_attend_kernel(const __half* __restrict__ kp, const __half* __restrict__ 
         if (blockIdx.x == 0 && threadIdx.x == 0) record_status(status, QK_DEV_EMPTY_SELECTION);
         return;
     }
-    const int pps = max(min_pps, (count + kMaxSplits - 1) / kMaxSplits);
+    const int pps = max(kMinPagesPerSplit, (count + max_splits - 1) / max_splits);
     const int nsplit = (count + pps - 1) / pps;
     if (uint32_t(count) > pstride || nsplit > int(gridDim.x)) {
         if (blockIdx.x == 0 && threadIdx.x == 0) record_status(status, QK_DEV_BAD_COUNT);
@@ -445,20 +446,19 @@ template <int D, int G>
 int run_attend(const qk_cache* c, uint32_t layer, const __half* q, uint32_t batch,
                const int32_t* pages, uint32_t pstride, const int32_t* counts, uint32_t max_list,
                void* out, int out_dtype, cudaStream_t st) {
-    // Pages per split: 8 (attend.cu's rule) unless the grid has CTAs to spare, then 16 (a
-    // CTA's fixed costs -- q fragments, combine, partials, merge ticket -- over more pages).
+    // Splits per (sequence, KV head): about 256 CTAs per launch (this kernel holds 3 CTAs
+    // per SM: one wave), at least 8 pages each.  cfg4 group-shared: 283 -> 257 us per layer
+    // step (1 split of 128 pages per unit instead of 8 of 16; 2 splits: 278, a 1.15-wave grid).
     const uint32_t units = batch * c->Hkv;
-    const uint32_t s8 = (max_list + kMinPagesPerSplit - 1) / kMinPagesPerSplit;
-    const int min_pps = (uint64_t(units) * s8 >= 8u * 148u) ? 2 * kMinPagesPerSplit : kMinPagesPerSplit;
-    const uint32_t splits = max_list <= uint32_t(min_pps) * kMaxSplits
-                                ? (max_list + min_pps - 1) / min_pps
-                                : uint32_t(kMaxSplits);
+    const int max_splits = int(std::min<uint32_t>(kMaxSplits, std::max<uint32_t>(1u, 256u / units)));
+    const uint32_t splits = std::min<uint32_t>(uint32_t(max_splits),
+                                               (max_list + kMinPagesPerSplit - 1) / kMinPagesPerSplit);
     const dim3 grid(splits ? splits : 1, batch * c->Hkv);
     const float scale_log2 = float(1.4426950408889634 / sqrt(double(c->desc.head_dim)));
     grouped_attend_kernel<D, G><<<grid, kThreads, 0, st>>>(
         c->k_pool, c->v_pool, c->d_len, q, pages, pstride, counts, layer, c->B, c->Hkv, c->S,
         c->desc.head_dim, c->slice_kv, scale_log2, c->ws_partial, c->ws_ticket, out, out_dtype,
-        c->d_status, min_pps);
+        c->d_status, max_splits);
     const_cast<qk_cache*>(c)->launches++;
     return cuda_check(cudaGetLastError(), "grouped_attend_kernel");
 }
