@@ -126,7 +126,7 @@ __global__ void prefill_kernel(__half* __restrict__ kp, __half* __restrict__ vp,
 // Every thread walks its page's new rows in token order with append's strict compares on
 // its 8 channels (the same first-seen semantics as the scalar kernel), all rows' loads in
 // flight first; the page record is reduced over the page's D/8 threads with shuffles.
-constexpr int kPfThreads = 128;
+constexpr int kPfThreads = 256;  // 16 pages per CTA at D=128: 238 -> 219 us at cfg2 (64: 237, 512: 229)
 
 template <int D>
 __global__ void __launch_bounds__(kPfThreads)
