@@ -97,6 +97,15 @@ estimate_mha_kernel(const __half* __restrict__ meta, const uint32_t* __restrict_
 
     const size_t s = (size_t(layer) * B + b) * Hkv + kvh;
     const __half* mslice = meta + s * slice_meta;  // [2][D][mrow]
+    if (tid < D) {
+        // One L2 bulk prefetch per channel of this CTA's sign-selected row segment ahead of
+        // the register loads (tools/microbench_meta.cu pattern F): 7.35 -> 6.84 us per cfg2
+        // layer, graph-timed.  (Inside the fused kernel the same prefetch loses.)
+        const uint32_t npg = min(uint32_t(kMhaPPC), ((P - page0) + 7u) & ~7u);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                         mslice + (size_t(need[tid]) * D + tid) * mrow + page0),
+                     "r"(npg * 2u) : "memory");
+    }
     const int cg = tid >> 5, pb = lane;            // warp = channel group: 512-byte loads
     const uint32_t pbase = page0 + uint32_t(pb) * 8;
     const bool act = pbase < P;
