@@ -40,6 +40,7 @@ constexpr int kThreads = 128;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxSplitPages = 256;  // page-list entries of a split staged in shared memory
 constexpr uint32_t kSplitTarget = 512;  // CTAs per launch the split rule aims at
+constexpr int kMinUnitsPerSplit = 16;     // pages (token mode: S-entry chunks) per split, at least
 
 template <int D>
 __global__ void __launch_bounds__(kThreads)
@@ -70,7 +71,7 @@ attend_kernel(const __half* __restrict__ kp, const __half* __restrict__ vp,
     }
     // Units of the split rule: pages, or chunks of S list entries (token mode).
     const int units = tokens ? int((uint32_t(count) + S - 1) / S) : count;
-    const int pps = max(kMinPagesPerSplit, (units + max_splits - 1) / max_splits);
+    const int pps = max(kMinUnitsPerSplit, (units + max_splits - 1) / max_splits);
     const int nsplit = (units + pps - 1) / pps;
     // A count past the list row, or needing more splits than the host launched, would read
     // past the row or never complete the merge ticket: reject it (uniform over the CTAs of
@@ -259,7 +260,7 @@ int run(const qk_cache* c, uint32_t layer, const __half* q, uint32_t batch,
     const uint32_t max_units = mode == kModeTokens ? (max_list + c->S - 1) / c->S : max_list;
     // Splits per row: about kSplitTarget CTAs per launch (one wave of a few CTAs per SM; a
     // CTA's fixed costs -- q, page list, combine, partials, merge ticket -- over as many pages
-    // as that allows), at least 8 units each.  Measured (cfg2 unless noted, µs per layer):
+    // as that allows), at least 16 units each (sparse cfg2: 16.3 -> 15.2 us against 8).  Measured (cfg2 unless noted, µs per layer):
     // dense 109 -> 88 (16 splits of 128 pages instead of 64 of 32), cfg4 per-head 366 -> 351
     // (1 split per row instead of 8), cfg5 unfused 111 -> 107 (2 instead of 8), sparse cfg2
     // unchanged (16 splits of 8).  A function of the launch's rows and the row's own count
@@ -268,7 +269,7 @@ int run(const qk_cache* c, uint32_t layer, const __half* q, uint32_t batch,
     const uint32_t rows = batch * c->Hq;
     const int max_splits = int(std::min<uint32_t>(kMaxSplits, std::max<uint32_t>(1u, kSplitTarget / rows)));
     const uint32_t splits_needed = std::min<uint32_t>(uint32_t(max_splits),
-                                                      (max_units + kMinPagesPerSplit - 1) / kMinPagesPerSplit);
+                                                      (max_units + kMinUnitsPerSplit - 1) / kMinUnitsPerSplit);
     const dim3 grid(splits_needed ? splits_needed : 1, batch * c->Hq);
     const float scale_log2 = float(1.4426950408889634 / sqrt(double(c->desc.head_dim)));
     attend_kernel<D><<<grid, kThreads, 0, st>>>(
