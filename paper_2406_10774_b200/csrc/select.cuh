@@ -597,7 +597,8 @@ __device__ void block_select_reg(const unsigned long long (&key)[KPT], uint32_t 
     const int nv = n > i0 ? int(min(uint32_t(KPT), n - i0)) : 0;  // valid keys of this thread
     uint4* hist4 = reinterpret_cast<uint4*>(sc.hist);
 
-    static_assert(KPT <= 16, "selbits holds 16 keys per thread");
+    static_assert(KPT <= 16 && 32 % KPT == 0,
+                  "selbits: a thread's keys lie in one 32-bit verdict word (KPT divides 32)");
 #pragma unroll
     for (int j = 0; j < BPL / 4; ++j) hist4[gt * (BPL / 4) + j] = make_uint4(0, 0, 0, 0);
     if (gt == 0) sc.n_cand = 0;

@@ -96,7 +96,6 @@ inline cudaError_t launch_topk_rows(uint32_t rows, uint32_t capacity, const doub
     // per-thread serial work of the radix pass halves; occupancy does not matter).
     if (rows <= 148u && capacity > 128u * 8u && capacity <= 512u * 8u) {
         if (capacity <= 256u * 8u) QK_TOPK_ROWS_K(256, 8);
-        else if (capacity <= 512u * 6u) QK_TOPK_ROWS_K(512, 6);
         else QK_TOPK_ROWS_K(512, 8);
     } else if (capacity <= 128u * kRowKpt) QK_TOPK_ROWS(128);
     else if (capacity <= 256u * kRowKpt) QK_TOPK_ROWS(256);
