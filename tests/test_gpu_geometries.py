@@ -220,3 +220,37 @@ def test_sparse_attend_rejects_overlong_count(qk):
     counts = torch.tensor([[8, 8]], dtype=torch.int32, device="cuda")
     qc.sparse_attend(0, q, pages, counts)
     qc.check_status()
+
+
+@pytest.mark.parametrize("L", [65536, 65552])
+def test_cfg4_geometry_bench_page_counts(qk, oracle_c, L):
+    """cfg4 at the page counts bench.py's timed steps reach: 4097 pages after the append
+    (4096 candidates: the row-pair top-K's half-CTA mode) and 4098 (4097 candidates: one
+    512-thread row at a time); wide GQA, so the separate kernels run."""
+    sample = [(0, 0), (3, 9), (17, 22), (31, 31)]
+    layer = DevLayer(qk, L, 32, 32, 8, L, sample)
+    q, out, pages, counts = layer.step(2048)
+    layer.check(oracle_c, q, out, pages, counts, 2048)
+
+
+@pytest.mark.parametrize("force", [True, False])
+def test_row_pair_topk_mixed_modes(qk, oracle_c, force):
+    """select_top_k rows paired across sequences (one query head per sequence): a pair whose
+    rows straddle the 4096-candidate bound takes the whole-CTA mode, the others the halves."""
+    rng = np.random.default_rng(4097)
+    d, Sz = 8, 16
+    lens = [65552, 40000, 65537, 65536, 100, 70000]
+    B = len(lens)
+    qc = qk.QuestCache(d, Sz, max_batch=B, num_q_heads=1, max_tokens=max(lens) + 16)
+    for b, L in enumerate(lens):
+        k = torch.zeros((1, L, d), dtype=torch.float16, device="cuda")
+        qc.prefill(0, b, k, k)
+    P = max((L + Sz - 1) // Sz for L in lens)
+    scores = torch.from_numpy(rng.standard_normal((B, 1, qc.max_pages))).cuda()
+    budget = 1024
+    pages, counts = qc.select_topk(0, scores, budget, force)
+    pages, counts, sc = pages.cpu().numpy(), counts.cpu().numpy(), scores.cpu().numpy()
+    for b, L in enumerate(lens):
+        Pb = (L + Sz - 1) // Sz
+        want = oracle_c.select_top_k(sc[b, 0, :Pb], Sz, budget, force)
+        assert pages[b, 0, :counts[b, 0]].tolist() == want.tolist(), b
