@@ -5,11 +5,12 @@
 // (sequence b = r / rows_per_seq, row h = r % rows_per_seq); its scores are the G score
 // rows starting at scores + (b * rows_per_seq + h) * G * sstride, combined per page by
 // `reduce` (G = 1: the row itself; G > 1: the GQA group score of grouped.cu -- max, or the
-// fp64 sum in head order).  Thread t of the NT-thread CTA holds the keys of candidates
-// [16t, 16t + 16) in registers and block_select_reg (select.cuh) selects exactly: one
+// fp64 sum in head order).  Thread t of an NT-thread group holds the keys of candidates
+// [KPT t, KPT t + KPT) in registers and block_select_reg (select.cuh) selects exactly: one
 // 11-bit radix pass on the 32-bit word past the keys' common prefix, the threshold bin
 // ranked by (key desc, page asc), heavy ties falling back to the 64-bit multi-pass routine.
-// NT * 16 >= the cache capacity, chosen on the host, so a captured graph stays valid.
+// The launch covers the cache capacity (NT * KPT >= capacity, or the row-pair kernel's
+// whole-CTA mode), chosen on the host, so a captured graph stays valid as contexts grow.
 #pragma once
 
 #include "select.cuh"
@@ -131,8 +132,9 @@ topk_row_pairs_kernel(const double* __restrict__ scores, uint32_t sstride,
     }
 }
 
-// Launches topk_rows_kernel with the smallest NT whose NT * 16 keys cover `capacity`
-// (<= kRowMaxPages; larger caches use topk.cu's shared-memory selection).
+// Launches the row top-K for `capacity` pages (<= kRowMaxPages; larger caches use topk.cu's
+// shared-memory selection): 8 keys per thread for launches of at most one row per SM, else
+// the smallest 128/256 x 16 CTA that covers the capacity, else the row-pair kernel.
 template <int G>
 inline cudaError_t launch_topk_rows(uint32_t rows, uint32_t capacity, const double* scores,
                                     uint32_t sstride, const int32_t* len, uint32_t layer,
